@@ -1,0 +1,969 @@
+// C ABI of libkkspgemm.so (include/kkspgemm.h) and the host orchestration of
+// the two phases.  The host takes exactly the decisions the reference takes
+// on the host (compression gate compression.cpp:131-147, resolve_config
+// engine.cpp:367-395, scans' totals engine.cpp:434-441); everything that
+// touches matrix data runs in the kernels of kk_kernels.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/kkspgemm.h"
+#include "kk_device.cuh"
+#include "kk_internal.h"
+
+namespace kk {
+long long launch_count();
+}
+
+using namespace kk;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ApiError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw ApiError{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what)
+{
+    if (e == cudaSuccess)
+        return;
+    if (e == cudaErrorMemoryAllocation)
+        fail(SPG_ERR_NOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(SPG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F> int guarded(F&& f)
+{
+    try {
+        f();
+        g_err.clear();
+        return SPG_OK;
+    } catch (const ApiError& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SPG_ERR_NOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SPG_ERR_INTERNAL;
+    }
+}
+
+void require_device()
+{
+    static int ok = [] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+            return 0;
+        // keep freed stream-ordered memory in the pool: repeated phases then
+        // allocate without touching the driver
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        return 1;
+    }();
+    if (!ok)
+        fail(SPG_ERR_CUDA, "no CUDA device: libkkspgemm has no CPU path");
+}
+
+int ceil_pow2_i(int64_t x)
+{
+    int64_t p = 1;
+    while (p < x)
+        p <<= 1;
+    return static_cast<int>(p);
+}
+
+int log2_i(int64_t p)
+{
+    int l = 0;
+    while ((int64_t{1} << l) < p)
+        ++l;
+    return l;
+}
+
+int host_bucket(unsigned long long x)
+{
+    if (x == 0)
+        return 0;
+    if (x == 1)
+        return 1;
+    return std::min(65 - __builtin_clzll(x - 1), 63);
+}
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+constexpr uint64_t kWarpSmemMax = 48 * 1024; // L1 accumulator budget per warp
+constexpr uint64_t kCtaSmem = 96 * 1024;     // two CTAs per SM
+
+// device-side allocation helper (stream ordered)
+template <class T> T* dalloc(size_t count, cudaStream_t st, const char* what)
+{
+    void* p = nullptr;
+    cuda_check(cudaMallocAsync(&p, std::max<size_t>(count * sizeof(T), 16), st), what);
+    return static_cast<T*>(p);
+}
+
+} // namespace
+
+namespace kk {
+
+TabLayout make_layout(int acc, int variant, int32_t S, int32_t domain, double occupancy,
+                      bool external_rows)
+{
+    TabLayout L;
+    L.acc = acc;
+    L.S = std::max<int32_t>(S, 1);
+    const uint64_t pb = variant == kVarNumeric ? 8 : 4;
+    L.has_ids = !external_rows;
+    L.has_pay = !external_rows && variant != kVarSymRaw;
+    uint64_t map_bytes = 0, aux_bytes = 0;
+    if (acc == kAccLP) {
+        const double occ = std::clamp(occupancy, 1e-6, 1.0);
+        const int64_t need = static_cast<int64_t>(std::ceil(L.S / occ));
+        L.T = std::max({ceil_pow2_i(need), ceil_pow2_i(int64_t{L.S} + 1), 32});
+        L.shift = 32 - log2_i(L.T);
+        map_bytes = 8ull * L.T;
+        aux_bytes = 4ull * L.S;
+    } else if (acc == kAccLL) {
+        L.T = std::max(ceil_pow2_i(L.S), 32);
+        L.shift = 32 - log2_i(L.T);
+        map_bytes = 4ull * L.T;
+        aux_bytes = 4ull * L.S;
+    } else {
+        L.T = std::max<int32_t>(domain, 1);
+        map_bytes = 4ull * L.T;
+    }
+    L.off_map = 0;
+    L.off_aux = static_cast<uint32_t>(align_up(map_bytes, 16));
+    L.off_ids = static_cast<uint32_t>(align_up(L.off_aux + aux_bytes, 16));
+    L.off_pay = static_cast<uint32_t>(align_up(L.off_ids + (L.has_ids ? 4ull * L.S : 0), 16));
+    L.bytes = align_up(L.off_pay + (L.has_pay ? pb * L.S : 0), 16);
+    return L;
+}
+
+} // namespace kk
+
+// ---------------------------------------------------------------------------
+// plans: row classes of one phase
+// ---------------------------------------------------------------------------
+namespace {
+
+struct PhaseClass {
+    TabLayout lay;
+    bool l2 = false;
+    int wpb = 8;
+    int grid = 0;
+    int64_t count = 0;
+    int64_t off = 0;
+};
+
+struct PhasePlan {
+    int acc = kAccLP;
+    bool flat = false;
+    int variant = kVarNumeric;
+    int32_t domain = 0;
+    std::vector<PhaseClass> classes;
+    BinParams bp{};
+    bool need_list = false; // more than one class: rows are binned
+    // L2 pool
+    uint64_t chunk_bytes = 0;
+    int32_t num_chunks = 0;
+    int pool_mode = 0;
+    int l2_class = -1;
+};
+
+// GPU meta-algorithm (PAPER.md:849-852 and Table tab:methods): kkmem (LL,
+// Thread-Sequential) when the average row flops are below the cutoff, kklp
+// (two-level LP, Thread-Flat-Parallel) otherwise.  A dense accumulator is used
+// when its map over the column domain is no larger than the hash table the
+// row bound needs and it fits the warp's L1 budget (column count vs max row
+// flops).  Forced configurations use the resolved choice as is.
+void device_choice(bool forced, const spg_resolved& rc, const spg_config& cfg, double avg_row_flops,
+                   int variant, int32_t domain, int64_t umax, int* acc, bool* flat)
+{
+    if (forced) {
+        *acc = rc.accumulator == SPG_ACC_LL ? kAccLL : rc.accumulator == SPG_ACC_DENSE ? kAccDense : kAccLP;
+        *flat = rc.scheme == SPG_SCHEME_FLAT_PARALLEL;
+        return;
+    }
+    if (avg_row_flops < cfg.avg_flops_cutoff) {
+        *acc = kAccLL;
+        *flat = false;
+    } else {
+        *acc = kAccLP;
+        *flat = true;
+    }
+    const int32_t s = static_cast<int32_t>(std::max<int64_t>(std::min<int64_t>(umax, domain), 1));
+    const TabLayout dense = make_layout(kAccDense, variant, s, domain, cfg.lp_max_occupancy, false);
+    const TabLayout hashed = make_layout(*acc, variant, s, domain, cfg.lp_max_occupancy, false);
+    if (dense.bytes <= hashed.bytes && dense.bytes <= kWarpSmemMax)
+        *acc = kAccDense;
+}
+
+int grid_for(int acc, bool flat, int variant, bool l2, int wpb, uint64_t smem, int64_t warps_needed)
+{
+    const int per_sm = row_kernel_max_blocks_per_sm(acc, flat, variant, l2, wpb, smem);
+    const int64_t want = (warps_needed + wpb - 1) / wpb;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sm_count())));
+}
+
+// hist: bucket counts of the unclamped row bounds; umax: exact max bound.
+PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsigned long long* hist,
+                     int64_t umax, const spg_config& cfg)
+{
+    PhasePlan P;
+    P.acc = acc;
+    P.flat = flat;
+    P.variant = variant;
+    P.domain = domain;
+    std::fill(std::begin(P.bp.bucket_class), std::end(P.bp.bucket_class), int8_t(-1));
+    const int dom_bucket = host_bucket(static_cast<unsigned long long>(std::max<int32_t>(domain, 0)));
+    const int64_t l1cap = cfg.l1_capacity > 0 ? cfg.l1_capacity : INT64_MAX;
+
+    // candidate L1 capacities (powers of two, the smallest covering 32 keys)
+    std::vector<int32_t> caps;
+    if (l1cap < 32) {
+        int32_t c = 1;
+        while (int64_t{c} * 2 <= l1cap)
+            c *= 2;
+        caps.push_back(c);
+    } else {
+        for (int32_t c = 32; int64_t{c} <= l1cap && c <= (1 << 20); c *= 2)
+            caps.push_back(c);
+    }
+    std::vector<int32_t> l1caps;
+    for (int32_t c : caps) {
+        const TabLayout L = make_layout(acc, variant, c, domain, cfg.lp_max_occupancy, false);
+        if (L.bytes <= kWarpSmemMax)
+            l1caps.push_back(c);
+    }
+
+    // bucket -> class
+    std::vector<int64_t> cls_count(l1caps.size() + 1, 0);
+    int8_t bc[64];
+    for (int b = 0; b < 64; ++b) {
+        bc[b] = -1;
+        const int be = std::min(b, dom_bucket);
+        if (be == 0)
+            continue;
+        const int64_t need = std::min<int64_t>(int64_t{1} << (be - 1), std::max<int32_t>(domain, 1));
+        int c = static_cast<int>(l1caps.size()); // L2
+        for (size_t q = 0; q < l1caps.size(); ++q)
+            if (l1caps[q] >= need) {
+                c = static_cast<int>(q);
+                break;
+            }
+        bc[b] = static_cast<int8_t>(c);
+        cls_count[c] += static_cast<int64_t>(hist[b]);
+    }
+    // compact to non-empty classes
+    std::vector<int> remap(cls_count.size(), -1);
+    int64_t off = 0;
+    for (size_t c = 0; c < cls_count.size(); ++c) {
+        if (cls_count[c] == 0)
+            continue;
+        PhaseClass pc;
+        pc.count = cls_count[c];
+        pc.off = off;
+        off += pc.count;
+        pc.l2 = c == l1caps.size();
+        if (!pc.l2) {
+            pc.lay = make_layout(acc, variant, l1caps[c], domain, cfg.lp_max_occupancy, false);
+            pc.wpb = static_cast<int>(std::clamp<uint64_t>(kCtaSmem / pc.lay.bytes, 1, 8));
+            pc.grid = grid_for(acc, flat, variant, false, pc.wpb, pc.wpb * pc.lay.bytes, pc.count);
+        } else {
+            const int32_t s = static_cast<int32_t>(std::max<int64_t>(std::min<int64_t>(umax, std::max<int32_t>(domain, 1)), 1));
+            pc.lay = make_layout(acc, variant, s, domain, cfg.lp_max_occupancy, variant == kVarNumeric);
+            P.chunk_bytes = align_up(pc.lay.bytes, 256);
+            if (static_cast<int64_t>(P.chunk_bytes) > cfg.pool_budget_bytes)
+                fail(SPG_ERR_POOL_SIZING, "plan_pool: a single chunk exceeds the memory budget");
+            const int64_t workers = std::min<int64_t>(pc.count, (int64_t)sm_count() * 16);
+            const int64_t by_budget = cfg.pool_budget_bytes / static_cast<int64_t>(P.chunk_bytes);
+            // memory_pool.cpp:83-109: one chunk per worker, 2x for many2many,
+            // shrink under the budget and fall back to many2many
+            int64_t chunks = cfg.pool_mode == SPG_POOL_ONE2ONE ? workers : 2 * workers;
+            P.pool_mode = cfg.pool_mode == SPG_POOL_ONE2ONE ? 0 : 1;
+            if (chunks > by_budget) {
+                chunks = std::max<int64_t>(1, by_budget);
+                if (chunks < workers)
+                    P.pool_mode = 1;
+            }
+            P.num_chunks = static_cast<int32_t>(chunks);
+            pc.wpb = 8;
+            const int64_t warps = P.pool_mode == 0 ? chunks : workers;
+            pc.grid = static_cast<int>((warps + pc.wpb - 1) / pc.wpb);
+            P.l2_class = static_cast<int>(P.classes.size());
+        }
+        remap[c] = static_cast<int>(P.classes.size());
+        P.classes.push_back(pc);
+    }
+    for (int b = 0; b < 64; ++b)
+        P.bp.bucket_class[b] = bc[b] >= 0 ? static_cast<int8_t>(remap[bc[b]]) : int8_t(-1);
+    for (size_t c = 0; c < P.classes.size() && c < 32; ++c)
+        P.bp.class_off[c] = P.classes[c].off;
+    P.need_list = P.classes.size() > 1;
+    if (P.classes.size() > 32)
+        fail(SPG_ERR_INTERNAL, "too many accumulator classes");
+    return P;
+}
+
+struct DevPool {
+    char* base = nullptr;
+    int* states = nullptr;
+    uint64_t bytes = 0;
+    int32_t chunks = 0;
+};
+
+void ensure_pool(DevPool& pool, const PhasePlan& P, cudaStream_t st)
+{
+    if (P.l2_class < 0)
+        return;
+    const uint64_t need = P.chunk_bytes * static_cast<uint64_t>(P.num_chunks);
+    if (pool.base && pool.bytes >= need && pool.chunks >= P.num_chunks)
+        return;
+    if (pool.base) {
+        cudaFreeAsync(pool.base, st);
+        cudaFreeAsync(pool.states, st);
+    }
+    pool.base = dalloc<char>(need, st, "pool");
+    pool.states = dalloc<int>(P.num_chunks, st, "pool states");
+    pool.bytes = need;
+    pool.chunks = P.num_chunks;
+    // all maps start empty (-1) and rows hand their chunk back clean
+    cuda_check(cudaMemsetAsync(pool.base, 0xFF, need, st), "pool init");
+    cuda_check(cudaMemsetAsync(pool.states, 0, sizeof(int) * P.num_chunks, st), "pool states");
+}
+
+void free_pool(DevPool& pool)
+{
+    if (pool.base)
+        cudaFree(pool.base);
+    if (pool.states)
+        cudaFree(pool.states);
+    pool = DevPool{};
+}
+
+struct PinnedBuf {
+    void* p = nullptr;
+    explicit PinnedBuf(size_t n)
+    {
+        if (cudaMallocHost(&p, n) != cudaSuccess)
+            fail(SPG_ERR_NOMEM, "pinned host buffer");
+    }
+    ~PinnedBuf() { cudaFreeHost(p); }
+};
+
+void validate_csr(const spg_csr* x, const char* name, bool need_vals)
+{
+    if (!x)
+        fail(SPG_ERR_CONTRACT, std::string(name) + ": null matrix");
+    if (x->num_rows < 0 || x->num_cols < 0 || x->nnz < 0)
+        fail(SPG_ERR_CONTRACT, std::string(name) + ": negative dimensions");
+    if (!x->row_offsets)
+        fail(SPG_ERR_CONTRACT, std::string(name) + ": null row_offsets");
+    if (x->nnz > 0 && !x->col_indices)
+        fail(SPG_ERR_CONTRACT, std::string(name) + ": null col_indices");
+    if (need_vals && x->nnz > 0 && !x->values)
+        fail(SPG_ERR_CONTRACT, std::string(name) + ": null values");
+}
+
+const char* dev_error_text(int code)
+{
+    switch (code) {
+    case kDevRowOverflow: return "numeric row exceeds the symbolic structure";
+    case kDevRowShort: return "numeric row shorter than the symbolic structure";
+    case kDevKeyRange: return "DenseAccumulator: key outside the column domain";
+    case kDevL2Overflow: return "level-2 accumulator overflow: chunk bound violated";
+    default: return "device error";
+    }
+}
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+// the handle
+// ---------------------------------------------------------------------------
+struct spg_handle {
+    spg_handle_info info{};
+    int64_t* d_rowptr = nullptr;
+    int64_t* d_prf = nullptr;
+    DevCounters* d_ctr = nullptr;
+    ScanTotals size_hist{};     // host copy of the row-size histogram
+    bool numeric_forced = false;
+    PhasePlan num;
+    int32_t* d_num_list = nullptr;
+    DevPool num_pool;
+    cudaStream_t stream = nullptr;
+
+    ~spg_handle()
+    {
+        if (d_rowptr)
+            cudaFree(d_rowptr);
+        if (d_prf)
+            cudaFree(d_prf);
+        if (d_ctr)
+            cudaFree(d_ctr);
+        if (d_num_list)
+            cudaFree(d_num_list);
+        free_pool(num_pool);
+    }
+};
+
+namespace {
+
+void build_numeric_plan(spg_handle* h, cudaStream_t st)
+{
+    const spg_config& cfg = h->info.config;
+    int acc;
+    bool flat;
+    device_choice(h->numeric_forced || cfg.accumulator != SPG_ACC_AUTO, h->info.numeric_choice, cfg,
+                  h->info.flops.avg_row_flops, kVarNumeric, h->info.k, h->info.max_row_size, &acc, &flat);
+    h->num = plan_phase(acc, flat, kVarNumeric, h->info.k, h->size_hist.hist, h->info.max_row_size, cfg);
+    if (h->d_num_list) {
+        cudaFreeAsync(h->d_num_list, st);
+        h->d_num_list = nullptr;
+    }
+    if (h->num.need_list) {
+        h->d_num_list = dalloc<int32_t>(std::max<int64_t>(h->info.m, 1), st, "numeric row list");
+        auto* fill = dalloc<unsigned long long>(32, st, "fill");
+        cuda_check(cudaMemsetAsync(fill, 0, 32 * sizeof(unsigned long long), st), "fill");
+        cuda_check(launch_bin_scatter(h->info.m, nullptr, h->d_rowptr, INT64_MAX, h->num.bp, fill,
+                                      h->d_num_list, st),
+                   "numeric binning");
+        cudaFreeAsync(fill, st);
+    }
+}
+
+int64_t row_offsets_base_and_end(const spg_csr* x, int64_t* host2)
+{
+    (void)x;
+    return host2[1] - host2[0];
+}
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* spg_last_error(void) { return g_err.c_str(); }
+
+int64_t spg_kernel_launch_count(void) { return kk::launch_count(); }
+
+int spg_config_init(spg_config* c)
+{
+    if (!c)
+        return SPG_ERR_CONTRACT;
+    // engine.hpp:18-31, memory_pool.hpp:88
+    c->scheme = SPG_SCHEME_SEQUENTIAL;
+    c->accumulator = SPG_ACC_AUTO;
+    c->l1_capacity = 0;
+    c->dense_cutoff_k = 250000;
+    c->avg_flops_cutoff = 256.0;
+    c->lp_max_occupancy = 0.5;
+    c->compression_gate = 0.15;
+    c->compression = SPG_COMPRESSION_AUTO;
+    c->collapse_divisor = 8;
+    c->worker_count = 1;
+    c->sort_output = 0;
+    c->row_block = 512;
+    c->pool_mode = SPG_POOL_ONE2ONE;
+    c->pool_budget_bytes = int64_t{1} << 30;
+    return SPG_OK;
+}
+
+int spg_resolve_config(int32_t phase, int32_t k, const spg_flops_stats* stats,
+                       const spg_compression_report* report, const spg_config* cfg,
+                       int64_t row_upper_bound, spg_resolved* out)
+{
+    return guarded([&] {
+        if (!stats || !report || !cfg || !out)
+            fail(SPG_ERR_CONTRACT, "resolve_config: null argument");
+        // engine.cpp:367-395
+        spg_resolved rc{};
+        const bool compressed = phase == SPG_PHASE_SYMBOLIC && report->applied;
+        rc.effective_k = compressed ? static_cast<int32_t>((int64_t{k} + 31) / 32) : k;
+        if (cfg->accumulator != SPG_ACC_AUTO) {
+            rc.accumulator = cfg->accumulator;
+            rc.scheme = cfg->scheme;
+        } else if (rc.effective_k < cfg->dense_cutoff_k) {
+            rc.accumulator = SPG_ACC_DENSE;
+            rc.scheme = cfg->scheme;
+        } else if (stats->avg_row_flops < cfg->avg_flops_cutoff) {
+            rc.accumulator = SPG_ACC_LL;
+            rc.scheme = cfg->scheme;
+        } else {
+            rc.accumulator = SPG_ACC_LP;
+            rc.scheme = SPG_SCHEME_FLAT_PARALLEL;
+        }
+        const int64_t bound = std::max<int64_t>(std::min<int64_t>(row_upper_bound, rc.effective_k), 1);
+        rc.l2_capacity = static_cast<int32_t>(bound);
+        rc.l1_capacity = cfg->l1_capacity > 0 ? cfg->l1_capacity : rc.l2_capacity;
+        *out = rc;
+    });
+}
+
+int spg_flat_position(const int64_t* prefix, int64_t len, int64_t t, int32_t* seg, int64_t* off)
+{
+    return guarded([&] {
+        if (!prefix || len < 1 || !seg || !off)
+            fail(SPG_ERR_CONTRACT, "flat_position: bad argument");
+        // engine.cpp:360-365: seg = upper_bound(prefix, t) - 1
+        const int64_t* it = std::upper_bound(prefix, prefix + len, t);
+        const int64_t s = (it - prefix) - 1;
+        *seg = static_cast<int32_t>(s);
+        *off = t - prefix[s];
+    });
+}
+
+int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, spg_handle_t* out,
+                 void* stream)
+{
+    spg_handle* h = nullptr;
+    const int rc = guarded([&] {
+        if (!out)
+            fail(SPG_ERR_CONTRACT, "symbolic: null output handle");
+        *out = nullptr;
+        validate_csr(a, "symbolic: A", false);
+        validate_csr(b, "symbolic: B", false);
+        if (a->num_cols != b->num_rows)
+            fail(SPG_ERR_CONTRACT, "symbolic: inner dimensions do not match"); // engine.cpp:399-400
+        require_device();
+        spg_config cfg;
+        if (cfg_in)
+            cfg = *cfg_in;
+        else
+            spg_config_init(&cfg);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        h = new spg_handle;
+        h->stream = st;
+        spg_handle_info& I = h->info;
+        I.config = cfg;
+        I.m = a->num_rows;
+        I.n = a->num_cols;
+        I.k = b->num_cols;
+        I.nnz_a = a->nnz;
+        I.nnz_b = b->nnz;
+        const int32_t m = I.m, n = I.n, k = I.k;
+
+        cudaEvent_t ev[3];
+        for (auto& e : ev)
+            cuda_check(cudaEventCreate(&e), "event");
+        struct EvGuard {
+            cudaEvent_t* e;
+            ~EvGuard()
+            {
+                for (int q = 0; q < 3; ++q)
+                    cudaEventDestroy(e[q]);
+            }
+        } evg{ev};
+
+        h->d_rowptr = dalloc<int64_t>(int64_t{m} + 1, st, "C row offsets");
+        h->d_prf = dalloc<int64_t>(std::max(m, 1), st, "per-row flops");
+        h->d_ctr = dalloc<DevCounters>(1, st, "counters");
+        I.d_c_row_offsets = h->d_rowptr;
+        I.d_per_row_flops = h->d_prf;
+        int64_t* d_prcf = dalloc<int64_t>(std::max(m, 1), st, "per-row cflops");
+        int32_t* d_csize = dalloc<int32_t>(std::max(n, 1), st, "csize");
+        // B slots hold the compressed pairs; index them like B (base-relative)
+        int64_t bview[2] = {0, 0}, aview[2] = {0, 0};
+        int32_t* d_csi_alloc = dalloc<int32_t>(std::max<int64_t>(b->nnz, 1), st, "csi");
+        uint32_t* d_cs_alloc = dalloc<uint32_t>(std::max<int64_t>(b->nnz, 1), st, "cs");
+        Totals* d_tot = dalloc<Totals>(1, st, "totals");
+        ScanTotals* d_stot = dalloc<ScanTotals>(1, st, "scan totals");
+
+        PinnedBuf pin(sizeof(Totals) + sizeof(ScanTotals) + sizeof(DevCounters) + 64);
+        auto* htot = static_cast<Totals*>(pin.p);
+        auto* hstot = reinterpret_cast<ScanTotals*>(htot + 1);
+        auto* hctr = reinterpret_cast<DevCounters*>(hstot + 1);
+        auto* hviews = reinterpret_cast<int64_t*>(hctr + 1);
+
+        cuda_check(cudaMemcpyAsync(hviews + 0, a->row_offsets, 8, cudaMemcpyDeviceToHost, st), "A view");
+        cuda_check(cudaMemcpyAsync(hviews + 1, a->row_offsets + m, 8, cudaMemcpyDeviceToHost, st), "A view");
+        cuda_check(cudaMemcpyAsync(hviews + 2, b->row_offsets, 8, cudaMemcpyDeviceToHost, st), "B view");
+        cuda_check(cudaMemcpyAsync(hviews + 3, b->row_offsets + n, 8, cudaMemcpyDeviceToHost, st), "B view");
+        cuda_check(cudaEventRecord(ev[0], st), "event");
+        cuda_check(cudaMemsetAsync(d_tot, 0, sizeof(Totals), st), "memset");
+        cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");
+        cuda_check(cudaMemsetAsync(h->d_ctr, 0, sizeof(DevCounters), st), "memset");
+        cuda_check(cudaStreamSynchronize(st), "views");
+        aview[0] = hviews[0];
+        aview[1] = hviews[1];
+        bview[0] = hviews[2];
+        bview[1] = hviews[3];
+        if (row_offsets_base_and_end(a, aview) != a->nnz || row_offsets_base_and_end(b, bview) != b->nnz)
+            fail(SPG_ERR_CONTRACT, "symbolic: nnz does not match row_offsets");
+        int32_t* d_csi = d_csi_alloc - bview[0];
+        uint32_t* d_cs = d_cs_alloc - bview[0];
+
+        // ---- K3 + K1/K4 ----
+        cuda_check(launch_compress(n, b->row_offsets, b->col_indices, d_csize, d_csi, d_cs, st), "compress");
+        const double avg_len = m > 0 ? static_cast<double>(a->nnz) / m : 0.0;
+        cuda_check(launch_flops(m, avg_len, a->row_offsets, a->col_indices, b->row_offsets, d_csize,
+                                h->d_prf, d_prcf, d_tot, st),
+                   "flops");
+        cuda_check(cudaMemcpyAsync(htot, d_tot, sizeof(Totals), cudaMemcpyDeviceToHost, st), "totals");
+        cuda_check(cudaEventRecord(ev[1], st), "event");
+        cuda_check(cudaStreamSynchronize(st), "flops sync");
+
+        // ---- host decisions (engine.cpp:409-423, compression.cpp:118-147) ----
+        I.flops.total_flops = static_cast<int64_t>(htot->total_f);
+        I.flops.max_row_flops = static_cast<int64_t>(htot->max_f);
+        I.flops.avg_degree_a = a->num_cols > 0 ? static_cast<double>(a->nnz) / a->num_cols : 0.0;
+        I.flops.avg_row_flops = m > 0 ? static_cast<double>(I.flops.total_flops) / m : 0.0;
+        I.avg_row_size_estimate = I.flops.avg_row_flops / std::max(cfg.collapse_divisor, 1);
+        spg_compression_report& R = I.compression;
+        R.compressed_flops = static_cast<int64_t>(htot->total_cf);
+        R.compressed_max_row_flops = static_cast<int64_t>(htot->max_cf);
+        R.cf = I.flops.total_flops > 0 ? static_cast<double>(R.compressed_flops) / I.flops.total_flops : 1.0;
+        R.cmrf = I.flops.max_row_flops > 0
+            ? static_cast<double>(R.compressed_max_row_flops) / I.flops.max_row_flops
+            : 1.0;
+        bool apply = false;
+        if (cfg.compression == SPG_COMPRESSION_ALWAYS)
+            apply = true;
+        else if (cfg.compression == SPG_COMPRESSION_NEVER)
+            apply = false;
+        else {
+            const int64_t threshold_ppm =
+                std::llround((1.0 - std::clamp(cfg.compression_gate, 0.0, 1.0)) * 1000000.0);
+            apply = I.flops.total_flops > 0
+                && R.compressed_flops * 1000000 < I.flops.total_flops * threshold_ppm;
+        }
+        R.applied = apply ? 1 : 0;
+        const int64_t raw_bound = apply ? R.compressed_max_row_flops : I.flops.max_row_flops;
+        cuda_check(spg_resolve_config(SPG_PHASE_SYMBOLIC, k, &I.flops, &R, &cfg, raw_bound, &I.symbolic_choice) == SPG_OK
+                       ? cudaSuccess
+                       : cudaErrorInvalidValue,
+                   "resolve_config");
+
+        // ---- K5: symbolic union ----
+        const int variant = apply ? kVarSymCompressed : kVarSymRaw;
+        const int32_t domain = I.symbolic_choice.effective_k;
+        int sacc;
+        bool sflat;
+        device_choice(cfg.accumulator != SPG_ACC_AUTO, I.symbolic_choice, cfg, I.flops.avg_row_flops, variant,
+                      domain, raw_bound, &sacc, &sflat);
+        const PhasePlan S =
+            plan_phase(sacc, sflat, variant, domain, apply ? htot->hist_cf : htot->hist_f, raw_bound, cfg);
+        cuda_check(cudaMemsetAsync(h->d_rowptr, 0, sizeof(int64_t) * (int64_t{m} + 1), st), "memset");
+        int32_t* d_list = nullptr;
+        if (S.need_list) {
+            d_list = dalloc<int32_t>(std::max(m, 1), st, "symbolic row list");
+            auto* fill = dalloc<unsigned long long>(32, st, "fill");
+            cuda_check(cudaMemsetAsync(fill, 0, 32 * sizeof(unsigned long long), st), "fill");
+            cuda_check(launch_bin_scatter(m, apply ? d_prcf : h->d_prf, nullptr, domain, S.bp, fill, d_list, st),
+                       "symbolic binning");
+            cudaFreeAsync(fill, st);
+        }
+        DevPool spool;
+        ensure_pool(spool, S, st);
+        for (const PhaseClass& pc : S.classes) {
+            RowLaunch L{};
+            L.a_rowptr = a->row_offsets;
+            L.a_cols = a->col_indices;
+            L.a_vals = nullptr;
+            L.b_rowptr = b->row_offsets;
+            L.b_cols = b->col_indices;
+            L.csize = d_csize;
+            L.csi = d_csi;
+            L.cs = d_cs;
+            L.list = S.need_list ? d_list + pc.off : nullptr;
+            L.nrows = S.need_list ? pc.count : m;
+            L.sym_sizes = h->d_rowptr + 1;
+            L.ctr = h->d_ctr;
+            L.lay = pc.lay;
+            L.wpb = pc.wpb;
+            L.grid = pc.grid;
+            L.l2 = pc.l2;
+            if (pc.l2)
+                L.pool = PoolDesc{spool.base, S.chunk_bytes, S.num_chunks, S.pool_mode, spool.states};
+            cuda_check(launch_row_kernel(L, S.acc, S.flat, S.variant, st), "symbolic kernel");
+        }
+        // ---- K2: scan ----
+        cuda_check(scan_sizes_inplace(h->d_rowptr, m, d_stot, st), "scan");
+        cuda_check(cudaMemcpyAsync(hstot, d_stot, sizeof(ScanTotals), cudaMemcpyDeviceToHost, st), "scan totals");
+        cuda_check(cudaMemcpyAsync(hctr, h->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, st), "counters");
+        int64_t* hnnz = hviews + 4;
+        cuda_check(cudaMemcpyAsync(hnnz, h->d_rowptr + m, 8, cudaMemcpyDeviceToHost, st), "nnz");
+        cuda_check(cudaEventRecord(ev[2], st), "event");
+        if (d_list)
+            cudaFreeAsync(d_list, st);
+        cudaFreeAsync(d_prcf, st);
+        cudaFreeAsync(d_csize, st);
+        cudaFreeAsync(d_csi_alloc, st);
+        cudaFreeAsync(d_cs_alloc, st);
+        cudaFreeAsync(d_tot, st);
+        cudaFreeAsync(d_stot, st);
+        if (spool.base) {
+            cudaFreeAsync(spool.base, st);
+            cudaFreeAsync(spool.states, st);
+        }
+        cuda_check(cudaStreamSynchronize(st), "symbolic sync");
+        if (hctr->error)
+            fail(SPG_ERR_INTERNAL, std::string("symbolic: ") + dev_error_text(hctr->error));
+
+        I.nnz_c = *hnnz;
+        I.max_row_size = static_cast<int64_t>(hstot->max_size);
+        I.avg_row_size = m > 0 ? static_cast<double>(I.nnz_c) / m : 0.0;
+        h->size_hist = *hstot;
+        float ms01 = 0.f, ms12 = 0.f;
+        cudaEventElapsedTime(&ms01, ev[0], ev[1]);
+        cudaEventElapsedTime(&ms12, ev[1], ev[2]);
+        I.compress_ms = ms01;
+        I.symbolic_stats.ms = ms12;
+        I.symbolic_stats.pool_allocations = static_cast<int64_t>(hctr->pool_allocations);
+        I.symbolic_stats.l2_inserts = static_cast<int64_t>(hctr->l2_inserts);
+        spg_resolve_config(SPG_PHASE_NUMERIC, k, &I.flops, &R, &cfg, I.max_row_size, &I.numeric_choice);
+        build_numeric_plan(h, st);
+        *out = h;
+    });
+    if (rc != SPG_OK) {
+        delete h;
+        if (out)
+            *out = nullptr;
+    }
+    return rc;
+}
+
+int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_cols, double* c_vals,
+                spg_phase_stats* stats, void* stream)
+{
+    return guarded([&] {
+        if (!h)
+            fail(SPG_ERR_CONTRACT, "numeric: null handle");
+        validate_csr(a, "numeric: A", true);
+        validate_csr(b, "numeric: B", true);
+        const spg_handle_info& I = h->info;
+        // engine.cpp:451-453
+        if (a->num_rows != I.m || a->num_cols != I.n || b->num_rows != I.n || b->num_cols != I.k
+            || a->nnz != I.nnz_a || b->nnz != I.nnz_b)
+            fail(SPG_ERR_REUSE, "numeric: operands do not match the symbolic handle");
+        if (I.nnz_c > 0 && (!c_cols || !c_vals))
+            fail(SPG_ERR_CONTRACT, "numeric: null output buffers");
+        require_device();
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        h->stream = st;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (stats) {
+            cuda_check(cudaEventCreate(&e0), "event");
+            cuda_check(cudaEventCreate(&e1), "event");
+            cuda_check(cudaEventRecord(e0, st), "event");
+        }
+        cuda_check(cudaMemsetAsync(h->d_ctr, 0, sizeof(DevCounters), st), "memset");
+        ensure_pool(h->num_pool, h->num, st);
+        const PhasePlan& P = h->num;
+        for (const PhaseClass& pc : P.classes) {
+            RowLaunch L{};
+            L.a_rowptr = a->row_offsets;
+            L.a_cols = a->col_indices;
+            L.a_vals = a->values;
+            L.b_rowptr = b->row_offsets;
+            L.b_cols = b->col_indices;
+            L.b_vals = b->values;
+            L.list = P.need_list ? h->d_num_list + pc.off : nullptr;
+            L.nrows = P.need_list ? pc.count : I.m;
+            L.c_rowptr = h->d_rowptr;
+            L.c_cols = c_cols;
+            L.c_vals = c_vals;
+            L.ctr = h->d_ctr;
+            L.lay = pc.lay;
+            L.wpb = pc.wpb;
+            L.grid = pc.grid;
+            L.l2 = pc.l2;
+            if (pc.l2)
+                L.pool = PoolDesc{h->num_pool.base, P.chunk_bytes, P.num_chunks, P.pool_mode, h->num_pool.states};
+            cuda_check(launch_row_kernel(L, P.acc, P.flat, kVarNumeric, st), "numeric kernel");
+        }
+        if (I.config.sort_output)
+            cuda_check(launch_sort_rows(I.m, h->d_rowptr, c_cols, c_vals, I.max_row_size, st), "sort_output");
+        if (stats) {
+            DevCounters hc{};
+            cuda_check(cudaEventRecord(e1, st), "event");
+            cuda_check(cudaMemcpyAsync(&hc, h->d_ctr, sizeof(hc), cudaMemcpyDeviceToHost, st), "counters");
+            cuda_check(cudaStreamSynchronize(st), "numeric sync");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            stats->ms = ms;
+            stats->pool_allocations = static_cast<int64_t>(hc.pool_allocations);
+            stats->l2_inserts = static_cast<int64_t>(hc.l2_inserts);
+            if (hc.error)
+                fail(SPG_ERR_INTERNAL, std::string("numeric: ") + dev_error_text(hc.error));
+        }
+    });
+}
+
+int spg_handle_info_get(spg_handle_t h, spg_handle_info* out)
+{
+    if (!h || !out)
+        return SPG_ERR_CONTRACT;
+    *out = h->info;
+    return SPG_OK;
+}
+
+int spg_handle_copy_row_offsets(spg_handle_t h, int64_t* host_dst)
+{
+    return guarded([&] {
+        if (!h || !host_dst)
+            fail(SPG_ERR_CONTRACT, "null argument");
+        cuda_check(cudaMemcpyAsync(host_dst, h->d_rowptr, sizeof(int64_t) * (int64_t{h->info.m} + 1),
+                                   cudaMemcpyDeviceToHost, h->stream),
+                   "copy row offsets");
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    });
+}
+
+int spg_handle_copy_per_row_flops(spg_handle_t h, int64_t* host_dst)
+{
+    return guarded([&] {
+        if (!h || !host_dst)
+            fail(SPG_ERR_CONTRACT, "null argument");
+        if (!h->d_prf)
+            fail(SPG_ERR_CONTRACT, "handle has no per-row flops (imported handle)");
+        cuda_check(cudaMemcpyAsync(host_dst, h->d_prf, sizeof(int64_t) * h->info.m, cudaMemcpyDeviceToHost,
+                                   h->stream),
+                   "copy per-row flops");
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    });
+}
+
+int spg_handle_copy_row_offsets_device(spg_handle_t h, int64_t* device_dst, void* stream)
+{
+    return guarded([&] {
+        if (!h || !device_dst)
+            fail(SPG_ERR_CONTRACT, "null argument");
+        cuda_check(cudaMemcpyAsync(device_dst, h->d_rowptr, sizeof(int64_t) * (int64_t{h->info.m} + 1),
+                                   cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)),
+                   "copy row offsets");
+    });
+}
+
+int spg_handle_set_numeric(spg_handle_t h, const spg_config* cfg, const spg_resolved* numeric_choice)
+{
+    return guarded([&] {
+        if (!h)
+            fail(SPG_ERR_CONTRACT, "null handle");
+        if (cfg)
+            h->info.config = *cfg;
+        if (numeric_choice) {
+            h->info.numeric_choice = *numeric_choice;
+            h->numeric_forced = true;
+        }
+        build_numeric_plan(h, h->stream);
+    });
+}
+
+int spg_handle_import(const spg_handle_desc* d, spg_handle_t* out, void* stream)
+{
+    spg_handle* h = nullptr;
+    const int rc = guarded([&] {
+        if (!d || !out || !d->c_row_offsets)
+            fail(SPG_ERR_CONTRACT, "import: null argument");
+        require_device();
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        h = new spg_handle;
+        h->stream = st;
+        spg_handle_info& I = h->info;
+        I.m = d->m;
+        I.n = d->n;
+        I.k = d->k;
+        I.nnz_a = d->nnz_a;
+        I.nnz_b = d->nnz_b;
+        I.nnz_c = d->c_row_offsets[d->m] - d->c_row_offsets[0];
+        I.flops = d->flops;
+        I.compression = d->compression;
+        I.max_row_size = d->max_row_size;
+        I.avg_row_size = d->avg_row_size;
+        I.avg_row_size_estimate = d->avg_row_size_estimate;
+        I.symbolic_choice = d->symbolic_choice;
+        I.numeric_choice = d->numeric_choice;
+        I.config = d->config;
+        I.symbolic_stats = d->symbolic_stats;
+        I.compress_ms = d->compress_ms;
+        h->d_rowptr = dalloc<int64_t>(int64_t{d->m} + 1, st, "C row offsets");
+        h->d_ctr = dalloc<DevCounters>(1, st, "counters");
+        I.d_c_row_offsets = h->d_rowptr;
+        I.d_per_row_flops = nullptr;
+        cuda_check(cudaMemcpyAsync(h->d_rowptr, d->c_row_offsets, sizeof(int64_t) * (int64_t{d->m} + 1),
+                                   cudaMemcpyHostToDevice, st),
+                   "upload row offsets");
+        ScanTotals* d_stot = dalloc<ScanTotals>(1, st, "hist");
+        cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");
+        cuda_check(launch_row_bucket_hist(d->m, h->d_rowptr, d_stot, st), "row hist");
+        cuda_check(cudaMemcpyAsync(&h->size_hist, d_stot, sizeof(ScanTotals), cudaMemcpyDeviceToHost, st), "hist");
+        cuda_check(cudaStreamSynchronize(st), "import sync");
+        cudaFreeAsync(d_stot, st);
+        I.max_row_size = std::max<int64_t>(I.max_row_size, static_cast<int64_t>(h->size_hist.max_size));
+        // the reference's numeric takes its choice from the handle as is
+        h->numeric_forced = true;
+        build_numeric_plan(h, st);
+        *out = h;
+    });
+    if (rc != SPG_OK) {
+        delete h;
+        if (out)
+            *out = nullptr;
+    }
+    return rc;
+}
+
+int spg_handle_check(spg_handle_t h)
+{
+    return guarded([&] {
+        if (!h)
+            fail(SPG_ERR_CONTRACT, "null handle");
+        DevCounters hc{};
+        cuda_check(cudaMemcpyAsync(&hc, h->d_ctr, sizeof(hc), cudaMemcpyDeviceToHost, h->stream), "counters");
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+        if (hc.error)
+            fail(SPG_ERR_INTERNAL, dev_error_text(hc.error));
+    });
+}
+
+void spg_handle_destroy(spg_handle_t h)
+{
+    if (h) {
+        cudaStreamSynchronize(h->stream);
+        delete h;
+    }
+}
+
+int spg_sort_rows(int32_t m, const int64_t* d_row_offsets, int32_t* d_cols, double* d_vals, void* stream)
+{
+    return guarded([&] {
+        require_device();
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        // max row size for the kernel's path choice
+        ScanTotals* d_stot = dalloc<ScanTotals>(1, st, "hist");
+        ScanTotals hs{};
+        cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");
+        cuda_check(launch_row_bucket_hist(m, d_row_offsets, d_stot, st), "row hist");
+        cuda_check(cudaMemcpyAsync(&hs, d_stot, sizeof(hs), cudaMemcpyDeviceToHost, st), "hist");
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        cudaFreeAsync(d_stot, st);
+        cuda_check(launch_sort_rows(m, d_row_offsets, d_cols, d_vals, static_cast<int64_t>(hs.max_size), st),
+                   "sort rows");
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,103 @@
+// Host-side declarations shared by the C ABI (kk_api.cu) and the kernel
+// launchers (kk_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kk {
+
+struct DevCounters;
+
+enum AccKind : int { kAccLL = 1, kAccLP = 2, kAccDense = 3 };
+enum RowVariant : int { kVarNumeric = 0, kVarSymRaw = 1, kVarSymCompressed = 2 };
+
+// Per-warp accumulator layout (bytes are relative to the warp's region).
+struct TabLayout {
+    int acc = kAccLP;
+    int32_t T = 0;     // LP slots / LL buckets / dense domain
+    int32_t S = 0;     // key capacity (first-touch positions)
+    int shift = 0;     // 32 - log2(T) for hashed maps
+    uint32_t off_map = 0, off_aux = 0, off_ids = 0, off_pay = 0;
+    uint64_t bytes = 0;
+    bool has_ids = true, has_pay = true;
+};
+
+TabLayout make_layout(int acc, int variant, int32_t S, int32_t domain, double occupancy,
+                      bool external_rows);
+
+struct Totals {
+    unsigned long long total_f, max_f, total_cf, max_cf;
+    unsigned long long hist_f[64];
+    unsigned long long hist_cf[64];
+};
+
+struct ScanTotals {
+    unsigned long long max_size;
+    unsigned long long hist[64];
+};
+
+struct PoolDesc {
+    char* base = nullptr;
+    uint64_t chunk_bytes = 0;
+    int32_t num_chunks = 0;
+    int32_t mode = 0; // 0 one2one, 1 many2many
+    int* states = nullptr;
+};
+
+struct RowLaunch {
+    // operands
+    const int64_t* a_rowptr;
+    const int32_t* a_cols;
+    const double* a_vals;
+    const int64_t* b_rowptr;
+    const int32_t* b_cols;
+    const double* b_vals;
+    const int32_t* csize;
+    const int32_t* csi;
+    const uint32_t* cs;
+    // rows
+    const int32_t* list; // nullptr: rows [0, nrows)
+    int64_t nrows;
+    // outputs
+    int64_t* sym_sizes;          // symbolic: sizes[i] (== rowptr + 1)
+    const int64_t* c_rowptr;     // numeric
+    int32_t* c_cols;
+    double* c_vals;
+    DevCounters* ctr;
+    // shape
+    TabLayout lay;
+    int wpb;
+    int grid;
+    bool l2;
+    PoolDesc pool;
+};
+
+// kernel launchers (kk_kernels.cu); each returns cudaGetLastError()
+cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
+                            int32_t* csize, int32_t* csi, uint32_t* cs, cudaStream_t st);
+cudaError_t launch_flops(int32_t m, double avg_len, const int64_t* a_rowptr,
+                         const int32_t* a_cols, const int64_t* b_rowptr, const int32_t* csize,
+                         int64_t* out_f, int64_t* out_cf, Totals* tot, cudaStream_t st);
+struct BinParams {
+    int8_t bucket_class[64];
+    int64_t class_off[32];
+};
+cudaError_t launch_bin_scatter(int32_t m, const int64_t* bound, const int64_t* rowptr_c,
+                               int64_t clamp, const BinParams& bp,
+                               unsigned long long* class_fill, int32_t* list, cudaStream_t st);
+cudaError_t launch_row_kernel(const RowLaunch& L, int acc, bool flat, int variant,
+                              cudaStream_t st);
+int row_kernel_max_blocks_per_sm(int acc, bool flat, int variant, bool l2, int wpb,
+                                 size_t smem);
+cudaError_t scan_sizes_inplace(int64_t* rowptr, int64_t m, ScanTotals* tot, cudaStream_t st);
+cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, double* vals,
+                             int64_t max_row, cudaStream_t st);
+cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals* tot,
+                                   cudaStream_t st);
+
+void count_launch(int n = 1);
+int sm_count();
+
+} // namespace kk

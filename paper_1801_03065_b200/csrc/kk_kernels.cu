@@ -1,0 +1,845 @@
+// sm_100a kernels of the kkSpGEMM hot path and their launchers.
+//
+//   compress_kernel      K3  compressed_row_sizes + compress_rows (compression.cpp:25-82)
+//   flops_kernel<G>      K1+K4 flops_stats + compressed flops (csr_matrix.cpp:136-154,
+//                             compression.cpp:109-117), with per-row bucket histograms
+//   bin_scatter_kernel        rows -> accumulator classes (row binning by bound)
+//   row_kernel<...>      K5/K6 symbolic / numeric row accumulation (engine.cpp:251-351)
+//   scan kernels         K2  device exclusive scan of row sizes (engine.cpp:434-438)
+//   sort kernels         K7  sort_output pass (engine.cpp:466-485)
+//
+// All of these are HBM/L2/latency-bound integer and fp64 scalar work; tensor
+// cores have no role.
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstdio>
+
+#include "kk_device.cuh"
+#include "kk_internal.h"
+
+namespace kk {
+
+namespace {
+std::atomic<long long> g_launches{0};
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
+
+int sm_count()
+{
+    static int sms = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return sms;
+}
+
+__device__ __forceinline__ int bucket_of(unsigned long long x)
+{
+    // 0 for x == 0, else ceil(log2 x) + 1: bucket b holds x in (2^(b-2), 2^(b-1)]
+    return x == 0 ? 0 : min(65 - __clzll(x - 1), 63);
+}
+
+// ---------------------------------------------------------------------------
+// K3: graph compression of B, written into B's own slots (pairs of row j at
+// [rowptr[j], rowptr[j] + csize[j])).  Warp per row.  Pair order is the
+// first-touch order of compression.cpp:67-73 for rows of <= 32 entries and
+// for sorted rows; unsorted long rows use an order-insensitive merge (the
+// compressed graph only feeds the order-independent bit-OR union).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t* __restrict__ rowptr,
+                                                       const int32_t* __restrict__ cols,
+                                                       int32_t* __restrict__ csize,
+                                                       int32_t* __restrict__ csi,
+                                                       uint32_t* __restrict__ cs)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += warps) {
+        const int64_t lo = __ldg(rowptr + j);
+        const int64_t len = __ldg(rowptr + j + 1) - lo;
+        if (len <= 32) {
+            const bool valid = lane < len;
+            const int32_t col = valid ? __ldg(cols + lo + lane) : 0;
+            const int32_t w = col >> 5;
+            const int32_t key = valid ? w : -1 - lane;
+            uint32_t orv = valid ? (1u << (col & 31)) : 0u;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_xor_sync(kFull, orv, off);
+                const int32_t ok = __shfl_xor_sync(kFull, key, off);
+                if (ok == key)
+                    orv |= o;
+            }
+            const uint32_t grp = __match_any_sync(kFull, key);
+            const bool leader = valid && (__ffs(grp) - 1) == lane;
+            const uint32_t lm = __ballot_sync(kFull, leader);
+            if (leader) {
+                const int pos = __popc(lm & lanemask_lt());
+                csi[lo + pos] = w;
+                cs[lo + pos] = orv;
+            }
+            if (lane == 0)
+                csize[j] = __popc(lm);
+            continue;
+        }
+        // long row: sortedness first (one extra read of the row, L1/L2 resident)
+        bool sorted = true;
+        int32_t prev_last = INT_MIN;
+        for (int64_t t0 = 0; t0 < len; t0 += 32) {
+            const bool valid = t0 + lane < len;
+            const int32_t c = valid ? __ldg(cols + lo + t0 + lane) : INT_MAX;
+            int32_t prev = __shfl_up_sync(kFull, c, 1);
+            if (lane == 0)
+                prev = prev_last;
+            sorted = sorted && __all_sync(kFull, !valid || c > prev);
+            prev_last = __shfl_sync(kFull, c, 31);
+        }
+        int32_t cnt = 0;
+        if (sorted) {
+            int32_t carry_w = -1;
+            for (int64_t t0 = 0; t0 < len; t0 += 32) {
+                const bool valid = t0 + lane < len;
+                const int32_t col = valid ? __ldg(cols + lo + t0 + lane) : 0;
+                const int32_t w = col >> 5;
+                const int32_t key = valid ? w : -1 - lane;
+                uint32_t orv = valid ? (1u << (col & 31)) : 0u;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t o = __shfl_xor_sync(kFull, orv, off);
+                    const int32_t ok = __shfl_xor_sync(kFull, key, off);
+                    if (ok == key)
+                        orv |= o;
+                }
+                int32_t pw = __shfl_up_sync(kFull, w, 1);
+                if (lane == 0)
+                    pw = carry_w;
+                const bool start = valid && w != pw;
+                if (valid && lane == 0 && w == carry_w)
+                    cs[lo + cnt - 1] |= orv; // run continues from the previous chunk
+                const uint32_t lm = __ballot_sync(kFull, start);
+                if (start) {
+                    const int pos = cnt + __popc(lm & lanemask_lt());
+                    csi[lo + pos] = w;
+                    cs[lo + pos] = orv;
+                }
+                cnt += __popc(lm);
+                const int last = static_cast<int>(len - 1 - t0 < 31 ? len - 1 - t0 : 31);
+                carry_w = __shfl_sync(kFull, w, last);
+                __syncwarp();
+            }
+        } else {
+            for (int64_t t0 = 0; t0 < len; t0 += 32) {
+                const bool valid = t0 + lane < len;
+                const int32_t col = valid ? __ldg(cols + lo + t0 + lane) : 0;
+                const int32_t w = col >> 5;
+                const int32_t key = valid ? w : -1 - lane;
+                uint32_t orv = valid ? (1u << (col & 31)) : 0u;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t o = __shfl_xor_sync(kFull, orv, off);
+                    const int32_t ok = __shfl_xor_sync(kFull, key, off);
+                    if (ok == key)
+                        orv |= o;
+                }
+                const uint32_t grp = __match_any_sync(kFull, key);
+                const bool leader = valid && (__ffs(grp) - 1) == lane;
+                int32_t found = -1;
+                if (leader)
+                    for (int32_t q = 0; q < cnt; ++q)
+                        if (csi[lo + q] == w) {
+                            found = q;
+                            break;
+                        }
+                __syncwarp();
+                const bool is_new = leader && found < 0;
+                const uint32_t nm = __ballot_sync(kFull, is_new);
+                if (is_new) {
+                    const int pos = cnt + __popc(nm & lanemask_lt());
+                    csi[lo + pos] = w;
+                    cs[lo + pos] = orv;
+                } else if (leader) {
+                    cs[lo + found] |= orv;
+                }
+                cnt += __popc(nm);
+                __syncwarp();
+            }
+        }
+        if (lane == 0)
+            csize[j] = cnt;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1+K4: per-row flops and compressed flops, totals, maxima and bucket
+// histograms (the histograms let the host size every accumulator class
+// without another pass).  G lanes per A row.
+// ---------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(256) flops_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,
+                                                    const int32_t* __restrict__ a_cols,
+                                                    const int64_t* __restrict__ b_rowptr,
+                                                    const int32_t* __restrict__ csize,
+                                                    int64_t* __restrict__ out_f,
+                                                    int64_t* __restrict__ out_cf, Totals* tot)
+{
+    __shared__ unsigned long long sh_hist[2][64];
+    for (int t = threadIdx.x; t < 128; t += blockDim.x)
+        (&sh_hist[0][0])[t] = 0;
+    __syncthreads();
+    const int glane = threadIdx.x & (G - 1);
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+    unsigned long long my_tf = 0, my_mf = 0, my_tcf = 0, my_mcf = 0;
+    const int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
+    // uniform trip count per warp so the group shuffles stay converged
+    const int64_t iters = (m + groups - 1) / groups;
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t i = first + it * groups;
+        int64_t f = 0, cf = 0;
+        if (i < m) {
+            const int64_t beg = __ldg(a_rowptr + i), end = __ldg(a_rowptr + i + 1);
+            for (int64_t p = beg + glane; p < end; p += G) {
+                const int32_t j = __ldg(a_cols + p);
+                f += __ldg(b_rowptr + j + 1) - __ldg(b_rowptr + j);
+                cf += __ldg(csize + j);
+            }
+        }
+#pragma unroll
+        for (int off = G / 2; off >= 1; off >>= 1) {
+            f += __shfl_xor_sync(kFull, f, off, G);
+            cf += __shfl_xor_sync(kFull, cf, off, G);
+        }
+        if (glane == 0 && i < m) {
+            out_f[i] = f;
+            out_cf[i] = cf;
+            my_tf += f;
+            my_tcf += cf;
+            my_mf = max(my_mf, (unsigned long long)f);
+            my_mcf = max(my_mcf, (unsigned long long)cf);
+            atomicAdd(&sh_hist[0][bucket_of(f)], 1ull);
+            atomicAdd(&sh_hist[1][bucket_of(cf)], 1ull);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        my_tf += __shfl_xor_sync(kFull, my_tf, off);
+        my_tcf += __shfl_xor_sync(kFull, my_tcf, off);
+        my_mf = max(my_mf, __shfl_xor_sync(kFull, my_mf, off));
+        my_mcf = max(my_mcf, __shfl_xor_sync(kFull, my_mcf, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&tot->total_f, my_tf);
+        atomicAdd(&tot->total_cf, my_tcf);
+        atomicMax(&tot->max_f, my_mf);
+        atomicMax(&tot->max_cf, my_mcf);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
+        const unsigned long long v = (&sh_hist[0][0])[t];
+        if (v)
+            atomicAdd(t < 64 ? &tot->hist_f[t] : &tot->hist_cf[t - 64], v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Row binning: class id from the row bound (per-row flops, compressed flops
+// or, for the numeric phase, the exact row size), warp-aggregated append.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bin_scatter_kernel(int32_t m, const int64_t* __restrict__ bound,
+                                                          const int64_t* __restrict__ rowptr_c,
+                                                          int64_t clamp, BinParams bp,
+                                                          unsigned long long* fill,
+                                                          int32_t* __restrict__ list)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        int c = -1;
+        if (i < m) {
+            int64_t u = bound ? bound[i] : rowptr_c[i + 1] - rowptr_c[i];
+            u = min(u, clamp);
+            c = bp.bucket_class[bucket_of((unsigned long long)u)];
+        }
+        const int key = c >= 0 ? c : -1 - lane;
+        const uint32_t grp = __match_any_sync(kFull, key);
+        const int leader = __ffs(grp) - 1;
+        unsigned long long off = 0;
+        if (c >= 0 && lane == leader)
+            off = atomicAdd(&fill[c], (unsigned long long)__popc(grp));
+        off = __shfl_sync(kFull, off, leader);
+        if (c >= 0)
+            list[bp.class_off[c] + (int64_t)off + __popc(grp & lanemask_lt())] = (int32_t)i;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5/K6: the row accumulation kernel.  One warp per row of C; the accumulator
+// (key->position map + ids + payload) lives in the warp's shared-memory
+// region (L1) or in a pool chunk in HBM (L2).
+// ---------------------------------------------------------------------------
+template <int kAcc> struct MapOf;
+template <> struct MapOf<kAccLP> {
+    using type = LPMap;
+    __device__ static LPMap make(unsigned char* r, const TabLayout& L, const int32_t*, DevCounters*)
+    {
+        return LPMap{reinterpret_cast<int2*>(r + L.off_map), reinterpret_cast<int32_t*>(r + L.off_aux),
+                     static_cast<uint32_t>(L.T - 1), L.shift};
+    }
+    __device__ static void init(unsigned char* r, const TabLayout& L, int lane)
+    {
+        int2* s = reinterpret_cast<int2*>(r + L.off_map);
+        for (int t = lane; t < L.T; t += 32)
+            s[t] = make_int2(kEmpty, 0);
+    }
+};
+template <> struct MapOf<kAccLL> {
+    using type = LLMap;
+    __device__ static LLMap make(unsigned char* r, const TabLayout& L, const int32_t* ids, DevCounters*)
+    {
+        return LLMap{reinterpret_cast<int32_t*>(r + L.off_map), reinterpret_cast<int32_t*>(r + L.off_aux),
+                     ids, L.shift};
+    }
+    __device__ static void init(unsigned char* r, const TabLayout& L, int lane)
+    {
+        int32_t* b = reinterpret_cast<int32_t*>(r + L.off_map);
+        for (int t = lane; t < L.T; t += 32)
+            b[t] = kEmpty;
+    }
+};
+template <> struct MapOf<kAccDense> {
+    using type = DenseMap;
+    __device__ static DenseMap make(unsigned char* r, const TabLayout& L, const int32_t*, DevCounters* c)
+    {
+        return DenseMap{reinterpret_cast<int32_t*>(r + L.off_map), L.T, c};
+    }
+    __device__ static void init(unsigned char* r, const TabLayout& L, int lane)
+    {
+        int32_t* b = reinterpret_cast<int32_t*>(r + L.off_map);
+        for (int t = lane; t < L.T; t += 32)
+            b[t] = kEmpty;
+    }
+};
+
+__device__ __forceinline__ int acquire_chunk(const PoolDesc& pool, int hint, int lane)
+{
+    int c = -1;
+    if (lane == 0) {
+        for (;;) {
+            for (int s = 0; s < pool.num_chunks; ++s) {
+                const int cc = (hint + s) % pool.num_chunks;
+                if (atomicCAS(&pool.states[cc], 0, 1) == 0) {
+                    c = cc;
+                    break;
+                }
+            }
+            if (c >= 0)
+                break;
+            __nanosleep(200);
+        }
+        __threadfence(); // also invalidates this SM's L1 (stale chunk lines)
+    }
+    return __shfl_sync(kFull, c, 0);
+}
+
+template <int kAcc, bool kFlat, int kVar, bool kL2>
+__global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    using Map = typename MapOf<kAcc>::type;
+    constexpr bool kNum = kVar == kVarNumeric;
+    constexpr bool kCountOnly = kVar == kVarSymRaw;
+    using P = typename std::conditional<kNum, double, uint32_t>::type;
+
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * L.wpb + wib;
+    int64_t nwarps = (int64_t)gridDim.x * L.wpb;
+    unsigned char* region = nullptr;
+    if constexpr (!kL2) {
+        region = smem + (size_t)wib * L.lay.bytes;
+        MapOf<kAcc>::init(region, L.lay, lane);
+        __syncwarp();
+    } else {
+        if (L.pool.mode == 0) {
+            if (gw >= L.pool.num_chunks)
+                return;
+            nwarps = L.pool.num_chunks;
+            region = reinterpret_cast<unsigned char*>(L.pool.base) + (size_t)gw * L.pool.chunk_bytes;
+        }
+    }
+
+    unsigned long long my_alloc = 0, my_inserts = 0;
+    for (int64_t r = gw; r < L.nrows; r += nwarps) {
+        const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        int chunk = -1;
+        if constexpr (kL2) {
+            if (L.pool.mode != 0) {
+                chunk = acquire_chunk(L.pool, static_cast<int>(gw % L.pool.num_chunks), lane);
+                region = reinterpret_cast<unsigned char*>(L.pool.base) + (size_t)chunk * L.pool.chunk_bytes;
+            }
+            ++my_alloc;
+        }
+        int32_t* ids;
+        P* pay;
+        int32_t cap;
+        int64_t cbase = 0;
+        if constexpr (kNum) {
+            cbase = __ldg(L.c_rowptr + i);
+            cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
+            if (cap == 0)
+                continue; // empty row of C: nothing to accumulate
+            if constexpr (kL2) {
+                ids = L.c_cols + cbase;
+                pay = reinterpret_cast<P*>(L.c_vals + cbase);
+            } else {
+                ids = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
+                pay = reinterpret_cast<P*>(region + L.lay.off_pay);
+            }
+        } else {
+            cap = L.lay.S;
+            ids = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
+            pay = reinterpret_cast<P*>(region + L.lay.off_pay);
+        }
+        Map map = MapOf<kAcc>::make(region, L.lay, ids, L.ctr);
+        int64_t products = 0;
+        int32_t cnt;
+        if constexpr (kVar == kVarNumeric) {
+            const NumericSource src{L.b_rowptr, L.b_cols, L.b_vals};
+            cnt = warp_row<kFlat, false>(L.a_rowptr, L.a_cols, L.a_vals, i, src, map, ids, pay,
+                                         cap, L.ctr, lane, products);
+        } else if constexpr (kVar == kVarSymRaw) {
+            const RawStructSource src{L.b_rowptr, L.b_cols};
+            cnt = warp_row<kFlat, true>(L.a_rowptr, L.a_cols, nullptr, i, src, map, ids, pay,
+                                        cap, L.ctr, lane, products);
+        } else {
+            const CompressedSource src{L.b_rowptr, L.csize, L.csi, L.cs};
+            cnt = warp_row<kFlat, false>(L.a_rowptr, L.a_cols, nullptr, i, src, map, ids, pay,
+                                         cap, L.ctr, lane, products);
+        }
+        const int32_t used = min(cnt, cap);
+        if constexpr (kNum) {
+            if (cnt < cap && lane == 0)
+                raise_error(L.ctr, kDevRowShort);
+            if constexpr (!kL2) {
+                for (int32_t q = lane; q < used; q += 32) {
+                    L.c_cols[cbase + q] = ids[q];
+                    L.c_vals[cbase + q] = pay[q];
+                }
+            }
+        } else {
+            int64_t size;
+            if constexpr (kCountOnly) {
+                size = cnt;
+            } else {
+                int64_t s = 0;
+                for (int32_t q = lane; q < used; q += 32)
+                    s += __popc(pay[q]);
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1)
+                    s += __shfl_xor_sync(kFull, s, off);
+                size = s;
+            }
+            if (lane == 0)
+                L.sym_sizes[i] = size;
+        }
+        if (kL2)
+            my_inserts += products;
+        __syncwarp();
+        for (int32_t q = lane; q < used; q += 32)
+            map.reset(q, ids);
+        __syncwarp();
+        if constexpr (kL2) {
+            if (chunk >= 0 && lane == 0) {
+                __threadfence();
+                atomicExch(&L.pool.states[chunk], 0);
+            }
+        }
+    }
+    if constexpr (kL2) {
+        if (lane == 0 && my_alloc) {
+            atomicAdd(&L.ctr->pool_allocations, my_alloc);
+            atomicAdd(&L.ctr->l2_inserts, my_inserts);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: in-place scan of row sizes.  rowptr[0] = 0 and rowptr[1..m] hold the
+// sizes on entry; on exit rowptr is the exclusive offset array.  Phase 1 also
+// records the max row size and the size-bucket histogram.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int64_t* __restrict__ x, int64_t n,
+                                                                   int64_t* __restrict__ block_sums,
+                                                                   ScanTotals* tot)
+{
+    __shared__ unsigned long long sh_hist[64];
+    __shared__ int64_t sh_red[kScanThreads / 32];
+    if (tot)
+        for (int t = threadIdx.x; t < 64; t += blockDim.x)
+            sh_hist[t] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    int64_t s = 0;
+    unsigned long long mx = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t idx = base + (int64_t)k * kScanThreads + threadIdx.x;
+        if (idx < n) {
+            const int64_t v = x[idx];
+            s += v;
+            if (tot) {
+                mx = max(mx, (unsigned long long)v);
+                atomicAdd(&sh_hist[bucket_of((unsigned long long)v)], 1ull);
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        s += __shfl_xor_sync(kFull, s, off);
+        mx = max(mx, __shfl_xor_sync(kFull, mx, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sh_red[threadIdx.x >> 5] = s;
+        if (tot)
+            atomicMax(&tot->max_size, mx);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < kScanThreads / 32; ++w)
+            t += sh_red[w];
+        block_sums[blockIdx.x] = t;
+    }
+    if (tot)
+        for (int t = threadIdx.x; t < 64; t += blockDim.x)
+            if (sh_hist[t])
+                atomicAdd(&tot->hist[t], sh_hist[t]);
+}
+
+// inclusive scan of one tile per block, plus an offset per block (or none)
+__global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(int64_t* __restrict__ x, int64_t n,
+                                                                 const int64_t* __restrict__ block_offsets)
+{
+    __shared__ int64_t sh_warp[kScanThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int64_t v[kScanItems];
+    int64_t run = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t idx = base + k;
+        v[k] = idx < n ? x[idx] : 0;
+        run += v[k];
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t incl = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int64_t y = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off)
+            incl += y;
+    }
+    if (lane == 31)
+        sh_warp[w] = incl;
+    __syncthreads();
+    int64_t wpre = 0;
+    for (int q = 0; q < w; ++q)
+        wpre += sh_warp[q];
+    int64_t acc = incl - run + wpre + (block_offsets ? block_offsets[blockIdx.x] : 0);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t idx = base + k;
+        acc += v[k];
+        if (idx < n)
+            x[idx] = acc;
+    }
+}
+
+// exclusive -> used as block offsets: shift an inclusive scan by one
+__global__ void shift_exclusive_kernel(const int64_t* __restrict__ incl, int64_t* __restrict__ excl, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        excl[i] = i == 0 ? 0 : incl[i - 1];
+}
+
+// inclusive scan of x[0..n) in place (recursive over tiles)
+static cudaError_t inclusive_scan(int64_t* x, int64_t n, ScanTotals* tot, cudaStream_t st)
+{
+    if (n <= 0)
+        return cudaSuccess;
+    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles == 1 && !tot) {
+        scan_tile_kernel<<<1, kScanThreads, 0, st>>>(x, n, nullptr);
+        count_launch();
+        return cudaGetLastError();
+    }
+    int64_t* sums = nullptr;
+    cudaError_t e = cudaMallocAsync(&sums, sizeof(int64_t) * 2 * tiles, st);
+    if (e != cudaSuccess)
+        return e;
+    int64_t* offs = sums + tiles;
+    scan_reduce_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(x, n, sums, tot);
+    count_launch();
+    e = inclusive_scan(sums, tiles, nullptr, st);
+    if (e == cudaSuccess) {
+        shift_exclusive_kernel<<<(unsigned)std::min<int64_t>((tiles + 255) / 256, 4096), 256, 0, st>>>(sums, offs, tiles);
+        scan_tile_kernel<<<(unsigned)tiles, kScanThreads, 0, st>>>(x, n, offs);
+        count_launch(2);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(sums, st);
+    return e;
+}
+
+cudaError_t scan_sizes_inplace(int64_t* rowptr, int64_t m, ScanTotals* tot, cudaStream_t st)
+{
+    // rowptr[0] is 0 already; scan the sizes in rowptr[1..m]
+    return inclusive_scan(rowptr + 1, m, tot, st);
+}
+
+__global__ void row_hist_kernel(int32_t m, const int64_t* __restrict__ rowptr, ScanTotals* tot)
+{
+    __shared__ unsigned long long sh_hist[64];
+    for (int t = threadIdx.x; t < 64; t += blockDim.x)
+        sh_hist[t] = 0;
+    __syncthreads();
+    unsigned long long mx = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long v = (unsigned long long)(rowptr[i + 1] - rowptr[i]);
+        mx = max(mx, v);
+        atomicAdd(&sh_hist[bucket_of(v)], 1ull);
+    }
+    atomicMax(&tot->max_size, mx);
+    __syncthreads();
+    for (int t = threadIdx.x; t < 64; t += blockDim.x)
+        if (sh_hist[t])
+            atomicAdd(&tot->hist[t], sh_hist[t]);
+}
+
+cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals* tot, cudaStream_t st)
+{
+    if (m <= 0)
+        return cudaSuccess;
+    const int blocks = (int)std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 8);
+    row_hist_kernel<<<blocks, 256, 0, st>>>(m, rowptr, tot);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K7: per-row column sort (sort_output).  Warp per row; rows of up to
+// kSortSmem entries rank-sort in shared memory, longer rows rank-sort from a
+// global copy.
+// ---------------------------------------------------------------------------
+constexpr int kSortSmem = 1024;
+constexpr int kSortWarps = 4;
+
+__global__ void __launch_bounds__(32 * kSortWarps) sort_rows_kernel(int32_t m, const int64_t* __restrict__ rowptr,
+                                                                    int32_t* __restrict__ cols,
+                                                                    double* __restrict__ vals,
+                                                                    const int32_t* __restrict__ big_cols,
+                                                                    const double* __restrict__ big_vals)
+{
+    __shared__ int32_t sh_c[kSortWarps][kSortSmem];
+    __shared__ double sh_v[kSortWarps][kSortSmem];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t warps = (int64_t)gridDim.x * kSortWarps;
+    for (int64_t i = (int64_t)blockIdx.x * kSortWarps + w; i < m; i += warps) {
+        const int64_t lo = rowptr[i];
+        const int64_t s = rowptr[i + 1] - lo;
+        if (s <= 1)
+            continue;
+        if (s <= kSortSmem) {
+            for (int64_t q = lane; q < s; q += 32) {
+                sh_c[w][q] = cols[lo + q];
+                sh_v[w][q] = vals[lo + q];
+            }
+            __syncwarp();
+            for (int64_t q = lane; q < s; q += 32) {
+                const int32_t c = sh_c[w][q];
+                int64_t rank = 0;
+                for (int64_t r = 0; r < s; ++r)
+                    rank += sh_c[w][r] < c;
+                cols[lo + rank] = c;
+                vals[lo + rank] = sh_v[w][q];
+            }
+            __syncwarp();
+        } else if (big_cols) {
+            for (int64_t q = lane; q < s; q += 32) {
+                const int32_t c = big_cols[lo + q];
+                int64_t rank = 0;
+                for (int64_t r = 0; r < s; ++r)
+                    rank += big_cols[lo + r] < c;
+                cols[lo + rank] = c;
+                vals[lo + rank] = big_vals[lo + q];
+            }
+        }
+    }
+}
+
+cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, double* vals,
+                             int64_t max_row, cudaStream_t st)
+{
+    if (m <= 0)
+        return cudaSuccess;
+    int32_t* bc = nullptr;
+    double* bv = nullptr;
+    int64_t nnz = 0;
+    if (max_row > kSortSmem) {
+        cudaMemcpyAsync(&nnz, rowptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        int64_t base = 0;
+        cudaMemcpyAsync(&base, rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        nnz -= base;
+        cudaError_t e = cudaMallocAsync(&bc, sizeof(int32_t) * nnz + 16, st);
+        if (e != cudaSuccess)
+            return e;
+        e = cudaMallocAsync(&bv, sizeof(double) * nnz + 16, st);
+        if (e != cudaSuccess)
+            return e;
+        // copies indexed like the originals (offset by the view's base)
+        cudaMemcpyAsync(bc, cols + base, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(bv, vals + base, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st);
+        bc -= base;
+        bv -= base;
+        const int blocks = (int)std::min<int64_t>((m + kSortWarps - 1) / kSortWarps, (int64_t)sm_count() * 16);
+        sort_rows_kernel<<<blocks, 32 * kSortWarps, 0, st>>>(m, rowptr, cols, vals, bc, bv);
+        count_launch();
+        cudaFreeAsync(bc + base, st);
+        cudaFreeAsync(bv + base, st);
+        return cudaGetLastError();
+    }
+    const int blocks = (int)std::min<int64_t>((m + kSortWarps - 1) / kSortWarps, (int64_t)sm_count() * 16);
+    sort_rows_kernel<<<blocks, 32 * kSortWarps, 0, st>>>(m, rowptr, cols, vals, nullptr, nullptr);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
+                            int32_t* csize, int32_t* csi, uint32_t* cs, cudaStream_t st)
+{
+    if (n <= 0)
+        return cudaSuccess;
+    const int blocks = (int)std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 8);
+    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flops(int32_t m, double avg_len, const int64_t* a_rowptr, const int32_t* a_cols,
+                         const int64_t* b_rowptr, const int32_t* csize, int64_t* out_f,
+                         int64_t* out_cf, Totals* tot, cudaStream_t st)
+{
+    if (m <= 0)
+        return cudaSuccess;
+    int g = 1;
+    while (g < 32 && g < avg_len)
+        g <<= 1;
+    const int rows_per_block = 256 / g;
+    const int blocks = (int)std::min<int64_t>((m + rows_per_block - 1) / rows_per_block, (int64_t)sm_count() * 8);
+#define KK_FLOPS(G)                                                                                   \
+    case G:                                                                                           \
+        flops_kernel<G><<<blocks, 256, 0, st>>>(m, a_rowptr, a_cols, b_rowptr, csize, out_f, out_cf, tot); \
+        break;
+    switch (g) {
+        KK_FLOPS(1)
+        KK_FLOPS(2)
+        KK_FLOPS(4)
+        KK_FLOPS(8)
+        KK_FLOPS(16)
+        KK_FLOPS(32)
+    }
+#undef KK_FLOPS
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bin_scatter(int32_t m, const int64_t* bound, const int64_t* rowptr_c,
+                               int64_t clamp, const BinParams& bp, unsigned long long* fill,
+                               int32_t* list, cudaStream_t st)
+{
+    if (m <= 0)
+        return cudaSuccess;
+    const int blocks = (int)std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 8);
+    bin_scatter_kernel<<<blocks, 256, 0, st>>>(m, bound, rowptr_c, clamp, bp, fill, list);
+    count_launch();
+    return cudaGetLastError();
+}
+
+namespace {
+template <int kAcc, bool kFlat, int kVar, bool kL2>
+const void* row_kernel_ptr()
+{
+    return reinterpret_cast<const void*>(&row_kernel<kAcc, kFlat, kVar, kL2>);
+}
+
+template <int kAcc, bool kFlat, int kVar>
+const void* pick_l2(bool l2)
+{
+    return l2 ? row_kernel_ptr<kAcc, kFlat, kVar, true>() : row_kernel_ptr<kAcc, kFlat, kVar, false>();
+}
+template <int kAcc, bool kFlat>
+const void* pick_var(int var, bool l2)
+{
+    switch (var) {
+    case kVarNumeric: return pick_l2<kAcc, kFlat, kVarNumeric>(l2);
+    case kVarSymRaw: return pick_l2<kAcc, kFlat, kVarSymRaw>(l2);
+    default: return pick_l2<kAcc, kFlat, kVarSymCompressed>(l2);
+    }
+}
+template <int kAcc>
+const void* pick_flat(bool flat, int var, bool l2)
+{
+    return flat ? pick_var<kAcc, true>(var, l2) : pick_var<kAcc, false>(var, l2);
+}
+const void* pick_kernel(int acc, bool flat, int var, bool l2)
+{
+    switch (acc) {
+    case kAccLL: return pick_flat<kAccLL>(flat, var, l2);
+    case kAccDense: return pick_flat<kAccDense>(flat, var, l2);
+    default: return pick_flat<kAccLP>(flat, var, l2);
+    }
+}
+} // namespace
+
+int row_kernel_max_blocks_per_sm(int acc, bool flat, int variant, bool l2, int wpb, size_t smem)
+{
+    const void* fn = pick_kernel(acc, flat, variant, l2);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, wpb * 32, smem) != cudaSuccess)
+        return 1;
+    return std::max(blocks, 1);
+}
+
+cudaError_t launch_row_kernel(const RowLaunch& L, int acc, bool flat, int variant, cudaStream_t st)
+{
+    if (L.nrows <= 0 || L.grid <= 0)
+        return cudaSuccess;
+    const void* fn = pick_kernel(acc, flat, variant, L.l2);
+    const size_t smem = L.l2 ? 0 : (size_t)L.wpb * L.lay.bytes;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return e;
+    }
+    void* args[] = {const_cast<RowLaunch*>(&L)};
+    cudaError_t e = cudaLaunchKernel(fn, dim3(L.grid), dim3(L.wpb * 32), args, smem, st);
+    count_launch();
+    return e;
+}
+
+} // namespace kk

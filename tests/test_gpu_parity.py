@@ -1,0 +1,292 @@
+"""GPU parity: libkkspgemm.so (sm_100a kernels, called through the C ABI)
+against the oracle and the reference's golden output.
+
+The contract (BASELINE.json north_star): C's row offsets and per-row sorted
+columns bit-exact, fp64 values within 1e-12 relative.  The kernels preserve the
+reference's first-touch column order and left-to-right summation order, so the
+tests below demand the stronger property — raw columns and value bits identical
+to the reference — and check the contractual one as well.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import csr_from_triplets, load_instances, random_csr
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12  # north_star: fp64 relative tolerance per entry
+
+
+def digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.fixture(scope="module")
+def kk():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1801_03065_b200 as kk
+    kk.lib()  # fails loudly when the extension is missing
+    return kk
+
+
+def run(kk, a, b, cfg=None):
+    res = kk.multiply(a, b, cfg)
+    c = res.c.to_host()
+    return res, c
+
+
+def assert_parity(oracle, a, b, c, exact=True):
+    ro = oracle.symbolic_row_offsets(a, b)
+    assert np.array_equal(c.row_offsets, ro), "row offsets differ"
+    cols, vals = oracle.numeric(a, b, ro)
+    # contractual: per-row sorted columns identical, values within 1e-12
+    sc, sv = oracle.sort_rows(ro, cols, vals)
+    gc, gv = oracle.sort_rows(ro, c.col_indices, c.values)
+    assert np.array_equal(sc, gc), "sorted columns differ"
+    assert oracle.max_rel_error(sv, gv) <= TOL
+    if exact:  # stronger: the reference's raw order and value bits
+        assert np.array_equal(c.col_indices, cols), "first-touch column order differs"
+        assert np.array_equal(c.values.view(np.int64), vals.view(np.int64)), "value bits differ"
+
+
+def test_hand_3x3(kk, oracle, kats):
+    k = kats["hand_3x3"]
+    a = csr_from_triplets(3, 3, k["a"])
+    b = csr_from_triplets(3, 3, k["b"])
+    for acc in (kk.AccumulatorKind.LL, kk.AccumulatorKind.LP, kk.AccumulatorKind.Dense):
+        cfg = kk.SpgemmConfig(accumulator=acc)
+        h = kk.symbolic(a, b, cfg)
+        assert h.c_row_offsets.tolist() == [0, 3, 4, 7]
+        assert h.nnz_c() == 7
+        c = kk.numeric(a, b, h).to_host()
+        assert c.col_indices.tolist() == k["reference_raw_cols"]
+        assert c.values.tolist() == k["reference_raw_vals"]
+
+
+def test_identity_and_empty_rows(kk, oracle):
+    eye = csr_from_triplets(10, 10, [(i, i, 1.0) for i in range(10)])
+    h = kk.symbolic(eye, eye)
+    assert h.c_row_offsets.tolist() == list(range(11))
+    assert h.max_row_size == 1
+    a = csr_from_triplets(3, 2, [(1, 0, 2.0)])
+    b = csr_from_triplets(2, 2, [(0, 1, 4.0)])
+    _, c = run(kk, a, b)
+    assert c.row_offsets.tolist() == [0, 0, 1, 1]
+    assert c.values.tolist() == [8.0]
+
+
+def test_cancellation_kept(kk, kats):
+    k = kats["cancellation"]
+    a = csr_from_triplets(*k["a_shape"], k["a"])
+    b = csr_from_triplets(*k["b_shape"], k["b"])
+    _, c = run(kk, a, b)
+    assert c.nnz() == 1 and c.values.tolist() == [0.0]
+
+
+def test_flops_and_compression_report(kk, oracle, kats):
+    k = kats["flops_5_0"]
+    a = csr_from_triplets(*k["a_shape"], k["a"])
+    b = csr_from_triplets(*k["b_shape"], k["b"])
+    h = kk.symbolic(a, b)
+    assert h.per_row_flops().tolist() == [5, 0]
+    assert h.flops.total_flops == 5 and h.flops.max_row_flops == 5
+    for name in ("gate_exact_15", "gate_16_of_20"):
+        g = kats[name]
+        b = csr_from_triplets(1, g["k"], [(0, c, 1.0) for c in g["b_cols"]])
+        a = csr_from_triplets(1, 1, [(0, 0, 1.0)])
+        h = kk.symbolic(a, b)
+        assert h.compression.compressed_flops == g["compressed_flops"]
+        assert h.compression.applied == g["applied"]
+
+
+def test_golden_instances(kk, oracle):
+    """The reference's own outputs (tests/golden/instances.npz), bit for bit."""
+    for inst in load_instances():
+        a, b = inst["a"], inst["b"]
+        res, c = run(kk, a, b)
+        h = res.handle
+        assert np.array_equal(h.per_row_flops(), inst["per_row_flops"])
+        assert h.flops.total_flops == inst["meta"]["total_flops"]
+        assert h.compression.compressed_flops == inst["meta"]["compressed_flops"]
+        assert h.compression.applied == bool(inst["meta"]["applied"])
+        assert h.max_row_size == inst["meta"]["max_row_size"]
+        assert h.symbolic_choice.accumulator == inst["meta"]["sym_acc"]
+        assert h.symbolic_choice.effective_k == inst["meta"]["sym_effk"]
+        assert h.numeric_choice.accumulator == inst["meta"]["num_acc"]
+        assert h.numeric_choice.l2_capacity == inst["meta"]["num_l2"]
+        assert np.array_equal(c.row_offsets, inst["c_ro"])
+        assert np.array_equal(c.col_indices, inst["c_ci"])
+        assert np.array_equal(c.values.view(np.int64), inst["c_v"].view(np.int64))
+
+
+@pytest.mark.parametrize("acc", [1, 2, 3])
+@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("l1", [0, 1, 40])
+def test_every_accumulator_scheme_and_level(kk, oracle, acc, scheme, l1):
+    """engine_test.cpp:76-135 / acceptance c1, c3: every accumulator x scheme,
+    with the level-1 table forced tiny so rows escalate to the HBM pool."""
+    if acc == 3 and l1 == 40:
+        pytest.skip("dense is single-level")
+    rng = np.random.default_rng(1000 * acc + 10 * scheme + l1)
+    allocs = 0
+    for it in range(6):
+        m, n, k = (int(x) for x in rng.integers(1, 150, 3))
+        a = random_csr(rng, m, n, 0.1, shuffle=bool(it % 2))
+        b = random_csr(rng, n, k, 0.1, shuffle=bool(it % 2))
+        cfg = kk.SpgemmConfig(accumulator=acc, scheme=scheme, l1_capacity=l1)
+        h = kk.symbolic(a, b, cfg)
+        st = kk.PhaseStats()
+        c = kk.numeric(a, b, h, st).to_host()
+        assert_parity(oracle, a, b, c)
+        allocs += h.symbolic_stats.pool_allocations + st.pool_allocations
+    if l1 == 1 and acc != 3:
+        assert allocs >= 1  # engine_test.cpp:118-119
+
+
+def test_ample_l1_never_touches_pool(kk):
+    rng = np.random.default_rng(67)
+    a = random_csr(rng, 50, 50, 0.1)
+    b = random_csr(rng, 50, 50, 0.1)
+    h = kk.symbolic(a, b, kk.SpgemmConfig(accumulator=kk.AccumulatorKind.LL))
+    st = kk.PhaseStats()
+    kk.numeric(a, b, h, st)
+    assert h.symbolic_stats.pool_allocations == 0 and st.pool_allocations == 0
+
+
+def test_compression_modes_agree(kk, oracle):
+    """engine_test.cpp:191-202 / acceptance c5."""
+    rng = np.random.default_rng(79)
+    for it in range(8):
+        a = random_csr(rng, 150, 150, 0.04 + 0.02 * (it % 3), shuffle=bool(it % 2))
+        b = random_csr(rng, 150, 150, 0.04, shuffle=bool(it % 2))
+        on = kk.symbolic(a, b, kk.SpgemmConfig(compression=kk.CompressionMode.Always))
+        off = kk.symbolic(a, b, kk.SpgemmConfig(compression=kk.CompressionMode.Never))
+        assert on.compression.applied and not off.compression.applied
+        assert np.array_equal(on.c_row_offsets, off.c_row_offsets)
+        assert np.array_equal(on.c_row_offsets, oracle.symbolic_row_offsets(a, b))
+
+
+def test_reuse_exact_and_linear(kk):
+    """engine_test.cpp:204-224: numeric(2A) == multiply(2A) bitwise, and 2x linearity."""
+    rng = np.random.default_rng(83)
+    a = random_csr(rng, 60, 60, 0.1)
+    b = random_csr(rng, 60, 60, 0.1)
+    h = kk.symbolic(a, b)
+    a2 = kk.CsrMatrix(a.num_rows, a.num_cols, a.row_offsets, a.col_indices, a.values * 2.0, True)
+    c_reuse = kk.numeric(a2, b, h).to_host()
+    c_fresh = kk.multiply(a2, b).c.to_host()
+    assert np.array_equal(c_reuse.col_indices, c_fresh.col_indices)
+    assert np.array_equal(c_reuse.values.view(np.int64), c_fresh.values.view(np.int64))
+    c_base = kk.numeric(a, b, h).to_host()
+    assert np.array_equal(c_reuse.values, 2.0 * c_base.values)
+
+
+def test_reuse_rejects_mismatch(kk):
+    rng = np.random.default_rng(89)
+    a = random_csr(rng, 30, 30, 0.2)
+    b = random_csr(rng, 30, 30, 0.2)
+    h = kk.symbolic(a, b)
+    wrong = random_csr(rng, 31, 30, 0.2)
+    with pytest.raises(kk.ReuseError):
+        kk.numeric(wrong, b, h)
+    trimmed = kk.CsrMatrix(a.num_rows, a.num_cols, a.row_offsets.copy(), a.col_indices, a.values, True)
+    trimmed.row_offsets[-1] -= 1
+    with pytest.raises(kk.ReuseError):
+        kk.numeric(trimmed, b, h)
+
+
+def test_contract_errors(kk):
+    a = csr_from_triplets(2, 3, [])
+    b = csr_from_triplets(2, 2, [])
+    with pytest.raises(kk.ContractError):
+        kk.symbolic(a, b)
+
+
+def test_sort_output(kk, oracle):
+    rng = np.random.default_rng(97)
+    a = random_csr(rng, 50, 50, 0.15)
+    b = random_csr(rng, 50, 50, 0.15)
+    c = kk.multiply(a, b, kk.SpgemmConfig(sort_output=True)).c.to_host()
+    assert c.sorted_rows
+    for i in range(c.num_rows):
+        seg = c.col_indices[c.row_offsets[i]:c.row_offsets[i + 1]]
+        assert np.all(np.diff(seg) > 0)
+    ro = oracle.symbolic_row_offsets(a, b)
+    sc, sv = oracle.sort_rows(ro, *oracle.numeric(a, b, ro))
+    assert np.array_equal(sc, c.col_indices)
+    assert np.array_equal(sv.view(np.int64), c.values.view(np.int64))
+
+
+def test_row_block_views(kk, oracle):
+    """Row shards (multi-GPU partitions) are row-offset views of one matrix."""
+    rng = np.random.default_rng(5)
+    a = random_csr(rng, 200, 120, 0.08)
+    b = random_csr(rng, 120, 90, 0.1)
+    da, db = a.to_device(), b.to_device()
+    ro = oracle.symbolic_row_offsets(a, b)
+    full_cols, full_vals = oracle.numeric(a, b, ro)
+    for lo, hi in ((0, 77), (77, 150), (150, 200)):
+        res = kk.multiply(da.row_block(lo, hi), db)
+        c = res.c.to_host()
+        assert np.array_equal(c.row_offsets, ro[lo:hi + 1] - ro[lo])
+        assert np.array_equal(c.col_indices, full_cols[ro[lo]:ro[hi]])
+        assert np.array_equal(c.values.view(np.int64), full_vals[ro[lo]:ro[hi]].view(np.int64))
+
+
+def test_triple_product(kk, oracle):
+    """engine_test.cpp:266-280: R*(A*P) with R = P^T, AP fed back unsorted."""
+    from paper_1801_03065_b200 import generators as G
+    a = G.laplace3d(10)
+    p = G.aggregation(10)
+    r = G.transpose(p)
+    ap = kk.multiply(a, p)
+    rap = kk.multiply(r, ap.c).c.to_host()
+    ro1 = oracle.symbolic_row_offsets(a, p)
+    apc, apv = oracle.numeric(a, p, ro1)
+    ap_host = kk.CsrMatrix(a.num_rows, p.num_cols, ro1, apc, apv, False)
+    assert_parity(oracle, r, ap_host, rap)
+
+
+CONFIG_CASES = ["c1_2d_n100", "c2_3d_n16", "c3_ap_n12", "c4_rmat_s10", "c5_3d_n20"]
+
+
+@pytest.mark.parametrize("name", CONFIG_CASES)
+def test_configs_reduced_vs_reference_digests(kk, config_golden, name):
+    """BASELINE configs at reduced scale: the reference's raw output digests."""
+    from paper_1801_03065_b200 import generators as G
+    make = {"c1_2d_n100": lambda: (G.laplace2d(100), None), "c2_3d_n16": lambda: (G.laplace3d(16), None),
+            "c3_ap_n12": lambda: (G.laplace3d(12), G.aggregation(12)),
+            "c4_rmat_s10": lambda: (G.rmat(10, 16, 1), None), "c5_3d_n20": lambda: (G.laplace3d(20), None)}
+    a, b = make[name]()
+    b = a if b is None else b
+    g = config_golden[name]
+    res, c = run(kk, a, b)
+    h = res.handle
+    assert h.flops.total_flops == g["total_flops"]
+    assert h.compression.compressed_flops == g["compressed_flops"]
+    assert h.symbolic_choice.accumulator == g["sym_acc"]
+    assert digest(c.row_offsets) == g["row_offsets_sha256"]
+    assert digest(c.col_indices) == g["raw_cols_sha256"]
+    assert digest(c.values) == g["raw_vals_sha256"]
+    if name == "c3_ap_n12":
+        r = G.transpose(b)
+        rap = kk.multiply(r, res.c).c.to_host()
+        g2 = config_golden["c3_rap_n12"]
+        assert digest(rap.row_offsets) == g2["row_offsets_sha256"]
+        assert digest(rap.col_indices) == g2["raw_cols_sha256"]
+        assert digest(rap.values) == g2["raw_vals_sha256"]
+
+
+def test_c1_full_size_vs_oracle(kk, oracle):
+    """Config 1 at full size (1M rows): bit-exact against the oracle."""
+    from paper_1801_03065_b200 import generators as G
+    a = G.laplace2d(1000)
+    _, c = run(kk, a, a)
+    assert c.nnz() == 12_980_004
+    assert_parity(oracle, a, a, c)
