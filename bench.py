@@ -1,0 +1,390 @@
+"""Benchmark: kkSpGEMM on B200 — BASELINE.json metric on config 2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config 2] [--scale 1.0] [--broadcast]
+
+A step is one full NoReuse multiply (symbolic + numeric, cli.cpp:137-151) of
+C = A*A, A = 3D 27-point Laplacian 160^3 (BASELINE configs[1]), fp64, inputs
+resident in HBM.  `value` is whole-job GFLOP/s = 2*flops/t (cli.cpp:124-128);
+the numeric-only (structure reuse) rate is reported beside it.  Under torchrun
+(N>1) rows of C are split into flop-balanced blocks, one per rank;
+B is resident on every rank (or broadcast over NCCL each step with
+--broadcast); time is the max over ranks of CUDA-event spans.
+
+Only the cpu_baseline leg and `--impl reference` execute the reference
+(oracle/_ref, compiled from its own sources) — as the measured CPU baseline,
+never on the GPU path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "GFLOP/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def workload(cfg: int, scale: float):
+    from paper_1801_03065_b200 import generators as G
+    if cfg == 1:
+        n = int(1000 * scale)
+        return G.laplace2d(n), f"c1: C=A*A, 2D 5-point Laplacian {n}^2, fp64"
+    if cfg == 2:
+        n = int(160 * scale)
+        return G.laplace3d(n), f"c2: C=A*A, 3D 27-point Laplacian {n}^3, fp64"
+    if cfg == 4:
+        return G.rmat(20, 16, 1), "c4: C=A*A, R-MAT scale 20 ef 16, fp64"
+    if cfg == 5:
+        n = int(200 * scale)
+        return G.laplace3d(n), f"c5: C=A*A, 3D 27-point Laplacian {n}^3, fp64"
+    raise SystemExit(f"config {cfg} is a parity-test case, not a bench line")
+
+
+def row_sample(a, every: int):
+    """Rows 0, every, 2*every, ... of A (rows of C are independent)."""
+    from paper_1801_03065_b200 import CsrMatrix
+    rows = np.arange(0, a.num_rows, every)
+    lo, hi = a.row_offsets[rows], a.row_offsets[rows + 1]
+    lens = hi - lo
+    ro = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(lens, out=ro[1:])
+    idx = np.concatenate([np.arange(l, h) for l, h in zip(lo, hi)]) if len(rows) else np.zeros(0, np.int64)
+    return CsrMatrix(len(rows), a.num_cols, ro, a.col_indices[idx], a.values[idx], True)
+
+
+def cpu_reference_rate(a, budget_s: float = 12.0, min_every: int = 4):
+    """Time the reference's own multiply (oracle/_ref) on a row sample of the
+    workload with all host threads.  Returns (gflops, cores, kind, sample)."""
+    cores = os.cpu_count() or 1
+    from oracle.oracle import Oracle, Reference, reference_available
+    o = Oracle()
+    if reference_available():
+        ref, kind = Reference(), "reference"
+    else:
+        ref, kind = None, "port"
+    # size the sample so one multiply takes ~budget/3
+    every = 256
+    while True:
+        s = row_sample(a, every)
+        _, fl, _ = o.flops_stats(s, a)
+        t0 = time.perf_counter()
+        if ref is not None:
+            ms, _ = ref.multiply_ms(s, a, worker_count=cores)
+            t = ms / 1e3
+        else:
+            o.multiply(s, a)
+            t = time.perf_counter() - t0
+        if t > budget_s / 3 or every <= min_every:
+            break
+        every = max(min_every, every // 4)
+    times = [t]
+    for _ in range(2):
+        if ref is not None:
+            ms, _ = ref.multiply_ms(s, a, worker_count=cores)
+            times.append(ms / 1e3)
+        else:
+            t0 = time.perf_counter()
+            o.multiply(s, a)
+            times.append(time.perf_counter() - t0)
+    tm = statistics.mean(times)
+    sample = (f"rows 0::{every} of A ({s.num_rows} rows, {fl} mults) times full B; mean of "
+              f"{len(times)} NoReuse multiplies, worker_count={cores if ref else 1}")
+    return 2.0 * fl / tm / 1e9, (cores if ref else 1), kind, sample
+
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.p is None:
+            return
+        time.sleep(0.25)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=5)
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_bytes_numeric(m, nnz_a, flops, nnz_c):
+    # SURVEY.md §8d Gustavson traffic model
+    return 16 * (m + 1) + 28 * nnz_a + 12 * flops + 12 * nnz_c
+
+
+def load_traffic(name: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(name)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kk", choices=["kk", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--broadcast", action="store_true", help="broadcast B over NCCL every step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    a_host, wl = workload(args.config, args.scale)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        rate, cores, kind, sample = cpu_reference_rate(a_host)
+        steps = []
+        for _ in range(args.warmup + args.steps):
+            steps.append(rate)
+        from oracle.oracle import Oracle
+        _, fl, _ = Oracle().flops_stats(a_host, a_host)
+        line = {"metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2.0 * fl / rate / 1e6,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": wl, "mode": "symbolic+numeric (NoReuse)"},
+                "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+                "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1801_03065_b200 as kk
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    A = a_host.to_device(dev)
+    B = A  # C = A*A
+    nnz_a = a_host.nnz()
+    m = a_host.num_rows
+
+    # ---- flop-balanced row partition, not timed ----
+    lo, hi = 0, m
+    if world > 1:
+        # per-row flops (sum of the referenced B row sizes) for the cut points
+        prf = torch.from_numpy(np.diff(a_host.row_offsets)).to(dev)
+        brs = (B.row_offsets[1:] - B.row_offsets[:-1])
+        rows_of = torch.repeat_interleave(torch.arange(m, device=dev), prf)
+        f = torch.zeros(m, dtype=torch.int64, device=dev).index_add_(0, rows_of, brs[A.col_indices.long()])
+        cum = torch.cumsum(f, 0)
+        total = int(cum[-1].item())
+        cuts = [0] + [int(torch.searchsorted(cum, total * g // world, right=False).item()) for g in range(1, world)] + [m]
+        lo, hi = cuts[rank], cuts[rank + 1]
+        del rows_of, f, cum, prf
+    A_shard = A.row_block(lo, hi)
+
+    # ---- warm-up and one reference multiply for counts ----
+    h0 = kk.symbolic(A_shard, B)
+    info = h0._info()
+    flops_local = int(info.flops.total_flops)
+    nnz_c_local = int(info.nnz_c)
+    cols = torch.empty(max(nnz_c_local, 1), dtype=torch.int32, device=dev)
+    vals = torch.empty(max(nnz_c_local, 1), dtype=torch.float64, device=dev)
+
+    def bcast_b():
+        if world > 1 and args.broadcast:
+            for t in (B.row_offsets, B.col_indices, B.values):
+                dist.broadcast(t, src=0)
+
+    def step_symnum():
+        bcast_b()
+        h = kk.symbolic(A_shard, B)
+        kk.numeric(A_shard, B, h, out=(cols, vals))
+        return h
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step_symnum()
+    barrier()
+
+    l0 = kk.kernel_launch_count()
+    with Clocks(local) as clk:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step_symnum()
+        ev1.record(stream)
+        barrier()
+    launches = kk.kernel_launch_count() - l0
+    ms_local = ev0.elapsed_time(ev1)
+
+    # ---- numeric-only (structure reuse): one symbolic, K numerics ----
+    for _ in range(args.warmup):
+        kk.numeric(A_shard, B, h0, out=(cols, vals))
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        bcast_b()
+        kk.numeric(A_shard, B, h0, out=(cols, vals))
+    e1.record(stream)
+    barrier()
+    ms_num_local = e0.elapsed_time(e1)
+    num_kernel_ms = ms_num_local / args.steps  # one row-kernel launch per numeric (single class)
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    ms = allmax(ms_local) / args.steps
+    ms_num = allmax(ms_num_local) / args.steps
+    flops = allsum(flops_local)
+    nnz_c = allsum(nnz_c_local)
+    value = 2.0 * flops / (ms / 1e3) / 1e9
+    value_num = 2.0 * flops / (ms_num / 1e3) / 1e9
+
+    # ---- end to end through the public API with host buffers (rank-local) ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+        lo_p, hi_p = int(a_host.row_offsets[lo]), int(a_host.row_offsets[hi])
+        h_ro = pin(a_host.row_offsets[lo:hi + 1] - lo_p)
+        h_ci = pin(a_host.col_indices[lo_p:hi_p])
+        h_v = pin(a_host.values[lo_p:hi_p])
+        hb_ro, hb_ci, hb_v = pin(a_host.row_offsets), pin(a_host.col_indices), pin(a_host.values)
+        o_ro = torch.empty(hi - lo + 1, dtype=torch.int64).pin_memory()
+        o_ci = torch.empty(max(nnz_c_local, 1), dtype=torch.int32).pin_memory()
+        o_v = torch.empty(max(nnz_c_local, 1), dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            da = kk.DeviceCsr(hi - lo, a_host.num_cols, h_ro.to(dev, non_blocking=True),
+                              h_ci.to(dev, non_blocking=True), h_v.to(dev, non_blocking=True), True, hi_p - lo_p)
+            db = kk.DeviceCsr(m, a_host.num_cols, hb_ro.to(dev, non_blocking=True),
+                              hb_ci.to(dev, non_blocking=True), hb_v.to(dev, non_blocking=True), True, nnz_a)
+            res = kk.multiply(da, db)
+            o_ro.copy_(res.c.row_offsets, non_blocking=True)
+            o_ci[:res.c.nnz()].copy_(res.c.col_indices, non_blocking=True)
+            o_v[:res.c.nnz()].copy_(res.c.values, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        ksteps = max(1, min(args.steps, 3))
+        t0.record(stream)
+        for _ in range(ksteps):
+            e2e_step()
+        t1.record(stream)
+        barrier()
+        ms_e2e = allmax(t0.elapsed_time(t1)) / ksteps
+        h2d = (h_ro.numel() * 8 + h_ci.numel() * 4 + h_v.numel() * 8 + hb_ro.numel() * 8 + hb_ci.numel() * 4
+               + hb_v.numel() * 8)
+        d2h = o_ro.numel() * 8 + nnz_c_local * 12
+        e2e = {"value": 2.0 * flops / (ms_e2e / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": int(allsum(h2d)), "d2h_bytes_per_step": int(allsum(d2h)),
+               "path": "kk.multiply (C ABI) with pinned host CSR in, host C out"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_kind = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    bytes_num = algorithmic_bytes_numeric(hi - lo, nnz_a if world == 1 else info.nnz_a, flops_local, nnz_c_local)
+    achieved = bytes_num / (num_kernel_ms / 1e3) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        rate, cores, kind, sample = cpu_reference_rate(a_host)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl, "mode": "symbolic+numeric (NoReuse multiply per step)",
+                   "m": m, "nnz_a": nnz_a, "flops": int(flops), "nnz_c": int(nnz_c),
+                   "parallelism": f"row-shard x{world}" + (" + NCCL broadcast of B" if args.broadcast else
+                                                            " (B resident)"),
+                   "l2_policy": "inputs larger than L2 (A = %.2f GB > 126 MB)" % (nnz_a * 12 / 1e9)},
+        "numeric_only": {"value": value_num, "unit": UNIT, "ms_per_step": ms_num},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": load_traffic(f"c{args.config}_numeric"),
+                     "kernel": "row_kernel (numeric)", "peak_kind": peak_kind,
+                     "algorithmic_bytes": bytes_num,
+                     "model": "16(m+1)+28nnzA+12flops+12nnzC (SURVEY §8d)"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -44,6 +44,25 @@ __device__ __forceinline__ int bucket_of(unsigned long long x)
     return x == 0 ? 0 : min(65 - __clzll(x - 1), 63);
 }
 
+// OR of v over the lanes of `grp` (a __match_any_sync group), every lane
+// receiving its own group's result.  Group membership is arbitrary, so the
+// members are visited one by one (rounds = largest group).
+__device__ __forceinline__ uint32_t group_or(uint32_t grp, uint32_t v, int lane)
+{
+    uint32_t acc = v;
+    uint32_t m = grp & ~(1u << lane);
+    const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(m)));
+    for (int r = 0; r < rounds; ++r) {
+        const int src = m ? __ffs(m) - 1 : lane;
+        const uint32_t x = __shfl_sync(kFull, v, src);
+        if (m) {
+            acc |= x;
+            m &= m - 1;
+        }
+    }
+    return acc;
+}
+
 // ---------------------------------------------------------------------------
 // K3: graph compression of B, written into B's own slots (pairs of row j at
 // [rowptr[j], rowptr[j] + csize[j])).  Warp per row.  Pair order is the
@@ -67,15 +86,8 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
             const int32_t col = valid ? __ldg(cols + lo + lane) : 0;
             const int32_t w = col >> 5;
             const int32_t key = valid ? w : -1 - lane;
-            uint32_t orv = valid ? (1u << (col & 31)) : 0u;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t o = __shfl_xor_sync(kFull, orv, off);
-                const int32_t ok = __shfl_xor_sync(kFull, key, off);
-                if (ok == key)
-                    orv |= o;
-            }
             const uint32_t grp = __match_any_sync(kFull, key);
+            const uint32_t orv = group_or(grp, valid ? (1u << (col & 31)) : 0u, lane);
             const bool leader = valid && (__ffs(grp) - 1) == lane;
             const uint32_t lm = __ballot_sync(kFull, leader);
             if (leader) {
@@ -107,14 +119,8 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
                 const int32_t col = valid ? __ldg(cols + lo + t0 + lane) : 0;
                 const int32_t w = col >> 5;
                 const int32_t key = valid ? w : -1 - lane;
-                uint32_t orv = valid ? (1u << (col & 31)) : 0u;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t o = __shfl_xor_sync(kFull, orv, off);
-                    const int32_t ok = __shfl_xor_sync(kFull, key, off);
-                    if (ok == key)
-                        orv |= o;
-                }
+                const uint32_t grp = __match_any_sync(kFull, key);
+                const uint32_t orv = group_or(grp, valid ? (1u << (col & 31)) : 0u, lane);
                 int32_t pw = __shfl_up_sync(kFull, w, 1);
                 if (lane == 0)
                     pw = carry_w;
@@ -138,15 +144,8 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
                 const int32_t col = valid ? __ldg(cols + lo + t0 + lane) : 0;
                 const int32_t w = col >> 5;
                 const int32_t key = valid ? w : -1 - lane;
-                uint32_t orv = valid ? (1u << (col & 31)) : 0u;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t o = __shfl_xor_sync(kFull, orv, off);
-                    const int32_t ok = __shfl_xor_sync(kFull, key, off);
-                    if (ok == key)
-                        orv |= o;
-                }
                 const uint32_t grp = __match_any_sync(kFull, key);
+                const uint32_t orv = group_or(grp, valid ? (1u << (col & 31)) : 0u, lane);
                 const bool leader = valid && (__ffs(grp) - 1) == lane;
                 int32_t found = -1;
                 if (leader)
