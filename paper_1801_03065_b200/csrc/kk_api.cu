@@ -168,24 +168,35 @@ namespace {
 struct PhaseClass {
     TabLayout lay;
     bool l2 = false;
+    bool fast = false;
     int wpb = 8;
     int grid = 0;
     int64_t count = 0;
     int64_t off = 0;
 };
 
+// level-2 (HBM pool) launch shape for rows whose bound is s_true
+struct L2Spec {
+    bool valid = false;
+    TabLayout lay;
+    uint64_t chunk_bytes = 0;
+    int32_t num_chunks = 0;
+    int pool_mode = 0;
+    int wpb = 8;
+    int grid = 0;
+};
+
 struct PhasePlan {
     int acc = kAccLP;
     bool flat = false;
+    bool fast = false;      // fast kernels (kk_fast.cu) for the L1 classes
+    bool optimistic = false; // L1 tables sized below the bound; overflow rows retry in L2
     int variant = kVarNumeric;
     int32_t domain = 0;
     std::vector<PhaseClass> classes;
     BinParams bp{};
     bool need_list = false; // more than one class: rows are binned
-    // L2 pool
-    uint64_t chunk_bytes = 0;
-    int32_t num_chunks = 0;
-    int pool_mode = 0;
+    L2Spec l2;
     int l2_class = -1;
 };
 
@@ -217,25 +228,80 @@ void device_choice(bool forced, const spg_resolved& rc, const spg_config& cfg, d
         *acc = kAccDense;
 }
 
-int grid_for(int acc, bool flat, int variant, bool l2, int wpb, uint64_t smem, int64_t warps_needed)
+// fast-kernel layouts (kk_fast.cu): numeric slots {key,pos,val} 16 B + slot_of;
+// symbolic slots {key,word} 8 B
+TabLayout make_layout_fast(int variant, int32_t S, double occupancy)
 {
-    const int per_sm = row_kernel_max_blocks_per_sm(acc, flat, variant, l2, wpb, smem);
-    const int64_t want = (warps_needed + wpb - 1) / wpb;
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sm_count())));
+    TabLayout L;
+    L.acc = kAccLP;
+    L.S = std::max<int32_t>(S, 1);
+    const double occ = std::clamp(occupancy, 1e-6, 1.0);
+    const int64_t need = static_cast<int64_t>(std::ceil(L.S / occ));
+    L.T = std::max({ceil_pow2_i(need), ceil_pow2_i(int64_t{L.S} + 1), 64});
+    L.shift = 32 - log2_i(L.T); // hash shift (kk_fast.cu)
+    if (variant == kVarNumeric) {
+        L.off_map = 0;                                          // vals  [T] double
+        L.off_ids = static_cast<uint32_t>(8ull * L.T);          // keys  [T] int32
+        L.off_aux = static_cast<uint32_t>(12ull * L.T);         // slot_of [S]
+        L.off_pay = static_cast<uint32_t>(align_up(12ull * L.T + 4ull * L.S, 16)); // step stage
+        L.bytes = L.off_pay + 896;
+    } else {
+        L.off_ids = 0;                                          // keys  [T]
+        L.off_map = static_cast<uint32_t>(4ull * L.T);          // words [T]
+        L.bytes = 8ull * L.T;
+    }
+    L.has_ids = false;
+    L.has_pay = false;
+    return L;
+}
+
+L2Spec plan_l2(int acc, int variant, int64_t s_true, int32_t domain, int64_t rows, const spg_config& cfg)
+{
+    L2Spec S;
+    S.valid = true;
+    const int32_t s = static_cast<int32_t>(std::max<int64_t>(std::min<int64_t>(s_true, std::max<int32_t>(domain, 1)), 1));
+    S.lay = make_layout(acc, variant, s, domain, cfg.lp_max_occupancy, variant == kVarNumeric);
+    S.chunk_bytes = align_up(S.lay.bytes, 256);
+    if (static_cast<int64_t>(S.chunk_bytes) > cfg.pool_budget_bytes)
+        fail(SPG_ERR_POOL_SIZING, "plan_pool: a single chunk exceeds the memory budget");
+    const int64_t workers = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sm_count() * 16));
+    const int64_t by_budget = cfg.pool_budget_bytes / static_cast<int64_t>(S.chunk_bytes);
+    // memory_pool.cpp:83-109: one chunk per worker (one2one) or 2x (many2many),
+    // halved under the budget, falling back to many2many below the worker count
+    int64_t chunks = cfg.pool_mode == SPG_POOL_ONE2ONE ? workers : 2 * workers;
+    S.pool_mode = cfg.pool_mode == SPG_POOL_ONE2ONE ? 0 : 1;
+    if (chunks > by_budget) {
+        chunks = std::max<int64_t>(1, by_budget);
+        if (chunks < workers)
+            S.pool_mode = 1;
+    }
+    S.num_chunks = static_cast<int32_t>(chunks);
+    S.wpb = 8;
+    const int64_t warps = S.pool_mode == 0 ? chunks : workers;
+    S.grid = static_cast<int>((warps + S.wpb - 1) / S.wpb);
+    return S;
 }
 
 // hist: bucket counts of the unclamped row bounds; umax: exact max bound.
+// fast: L1 classes run the kk_fast.cu kernels; opt_div > 0 sizes their tables
+// optimistically at 2*bound/opt_div keys (the reference's row-size estimate
+// flops/collapse_divisor, engine.cpp:410-411, with 2x headroom).
 PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsigned long long* hist,
-                     int64_t umax, const spg_config& cfg)
+                     int64_t umax, const spg_config& cfg, bool fast = false, int opt_div = 0)
 {
     PhasePlan P;
     P.acc = acc;
     P.flat = flat;
+    P.fast = fast;
     P.variant = variant;
     P.domain = domain;
     std::fill(std::begin(P.bp.bucket_class), std::end(P.bp.bucket_class), int8_t(-1));
     const int dom_bucket = host_bucket(static_cast<unsigned long long>(std::max<int32_t>(domain, 0)));
     const int64_t l1cap = cfg.l1_capacity > 0 ? cfg.l1_capacity : INT64_MAX;
+    auto layout_of = [&](int32_t c) {
+        return fast ? make_layout_fast(variant, c, cfg.lp_max_occupancy)
+                    : make_layout(acc, variant, c, domain, cfg.lp_max_occupancy, false);
+    };
 
     // candidate L1 capacities (powers of two, the smallest covering 32 keys)
     std::vector<int32_t> caps;
@@ -249,11 +315,9 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
             caps.push_back(c);
     }
     std::vector<int32_t> l1caps;
-    for (int32_t c : caps) {
-        const TabLayout L = make_layout(acc, variant, c, domain, cfg.lp_max_occupancy, false);
-        if (L.bytes <= kWarpSmemMax)
+    for (int32_t c : caps)
+        if (layout_of(c).bytes <= kWarpSmemMax)
             l1caps.push_back(c);
-    }
 
     // bucket -> class
     std::vector<int64_t> cls_count(l1caps.size() + 1, 0);
@@ -263,7 +327,14 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
         const int be = std::min(b, dom_bucket);
         if (be == 0)
             continue;
-        const int64_t need = std::min<int64_t>(int64_t{1} << (be - 1), std::max<int32_t>(domain, 1));
+        int64_t need = std::min<int64_t>(int64_t{1} << (be - 1), std::max<int32_t>(domain, 1));
+        if (fast && opt_div > 0) {
+            const int64_t est = std::max<int64_t>(32, ceil_pow2_i((2 * need + opt_div - 1) / opt_div));
+            if (est < need) {
+                need = est;
+                P.optimistic = true;
+            }
+        }
         int c = static_cast<int>(l1caps.size()); // L2
         for (size_t q = 0; q < l1caps.size(); ++q)
             if (l1caps[q] >= need) {
@@ -275,7 +346,7 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
     }
     // compact to non-empty classes
     std::vector<int> remap(cls_count.size(), -1);
-    int64_t off = 0;
+    int64_t off = 0, l2_rows = 0;
     for (size_t c = 0; c < cls_count.size(); ++c) {
         if (cls_count[c] == 0)
             continue;
@@ -285,34 +356,36 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
         off += pc.count;
         pc.l2 = c == l1caps.size();
         if (!pc.l2) {
-            pc.lay = make_layout(acc, variant, l1caps[c], domain, cfg.lp_max_occupancy, false);
+            pc.fast = fast;
+            pc.lay = layout_of(l1caps[c]);
             pc.wpb = static_cast<int>(std::clamp<uint64_t>(kCtaSmem / pc.lay.bytes, 1, 8));
-            pc.grid = grid_for(acc, flat, variant, false, pc.wpb, pc.wpb * pc.lay.bytes, pc.count);
+            const uint64_t smem = pc.wpb * pc.lay.bytes;
+            int per_sm;
+            if (!fast)
+                per_sm = row_kernel_max_blocks_per_sm(acc, flat, variant, false, pc.wpb, smem);
+            else if (variant == kVarNumeric)
+                per_sm = numeric_fast_blocks_per_sm(pc.wpb, smem);
+            else
+                per_sm = symbolic_fast_blocks_per_sm(variant == kVarSymCompressed, pc.wpb, smem);
+            const int64_t want = (pc.count + pc.wpb - 1) / pc.wpb;
+            pc.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sm_count())));
         } else {
-            const int32_t s = static_cast<int32_t>(std::max<int64_t>(std::min<int64_t>(umax, std::max<int32_t>(domain, 1)), 1));
-            pc.lay = make_layout(acc, variant, s, domain, cfg.lp_max_occupancy, variant == kVarNumeric);
-            P.chunk_bytes = align_up(pc.lay.bytes, 256);
-            if (static_cast<int64_t>(P.chunk_bytes) > cfg.pool_budget_bytes)
-                fail(SPG_ERR_POOL_SIZING, "plan_pool: a single chunk exceeds the memory budget");
-            const int64_t workers = std::min<int64_t>(pc.count, (int64_t)sm_count() * 16);
-            const int64_t by_budget = cfg.pool_budget_bytes / static_cast<int64_t>(P.chunk_bytes);
-            // memory_pool.cpp:83-109: one chunk per worker, 2x for many2many,
-            // shrink under the budget and fall back to many2many
-            int64_t chunks = cfg.pool_mode == SPG_POOL_ONE2ONE ? workers : 2 * workers;
-            P.pool_mode = cfg.pool_mode == SPG_POOL_ONE2ONE ? 0 : 1;
-            if (chunks > by_budget) {
-                chunks = std::max<int64_t>(1, by_budget);
-                if (chunks < workers)
-                    P.pool_mode = 1;
-            }
-            P.num_chunks = static_cast<int32_t>(chunks);
-            pc.wpb = 8;
-            const int64_t warps = P.pool_mode == 0 ? chunks : workers;
-            pc.grid = static_cast<int>((warps + pc.wpb - 1) / pc.wpb);
+            l2_rows = pc.count;
             P.l2_class = static_cast<int>(P.classes.size());
         }
         remap[c] = static_cast<int>(P.classes.size());
         P.classes.push_back(pc);
+    }
+    if (P.l2_class >= 0 || P.optimistic) {
+        // the HBM path runs the generic kernels (LP when the L1 ran the fast ones)
+        const int l2acc = fast ? kAccLP : acc;
+        P.l2 = plan_l2(l2acc, variant, umax, domain, P.optimistic ? std::max<int64_t>(l2_rows, sm_count() * 16) : l2_rows, cfg);
+        if (P.l2_class >= 0) {
+            PhaseClass& pc = P.classes[P.l2_class];
+            pc.lay = P.l2.lay;
+            pc.wpb = P.l2.wpb;
+            pc.grid = P.l2.grid;
+        }
     }
     for (int b = 0; b < 64; ++b)
         P.bp.bucket_class[b] = bc[b] >= 0 ? static_cast<int8_t>(remap[bc[b]]) : int8_t(-1);
@@ -331,9 +404,9 @@ struct DevPool {
     int32_t chunks = 0;
 };
 
-void ensure_pool(DevPool& pool, const PhasePlan& P, cudaStream_t st)
+void ensure_pool(DevPool& pool, const L2Spec& P, cudaStream_t st)
 {
-    if (P.l2_class < 0)
+    if (!P.valid)
         return;
     const uint64_t need = P.chunk_bytes * static_cast<uint64_t>(P.num_chunks);
     if (pool.base && pool.bytes >= need && pool.chunks >= P.num_chunks)
@@ -433,9 +506,24 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
     const spg_config& cfg = h->info.config;
     int acc;
     bool flat;
-    device_choice(h->numeric_forced || cfg.accumulator != SPG_ACC_AUTO, h->info.numeric_choice, cfg,
-                  h->info.flops.avg_row_flops, kVarNumeric, h->info.k, h->info.max_row_size, &acc, &flat);
-    h->num = plan_phase(acc, flat, kVarNumeric, h->info.k, h->size_hist.hist, h->info.max_row_size, cfg);
+    const bool forced = h->numeric_forced || cfg.accumulator != SPG_ACC_AUTO;
+    device_choice(forced, h->info.numeric_choice, cfg, h->info.flops.avg_row_flops, kVarNumeric, h->info.k,
+                  h->info.max_row_size, &acc, &flat);
+    bool fast = false;
+    if (!forced) {
+        // Auto on the GPU: the partitioning follows the average B-row length —
+        // Thread-Sequential (one B row per step, warp lanes over its entries)
+        // when rows fill a good part of the warp, Thread-Flat otherwise.
+        const double avg_b = h->info.n > 0 ? static_cast<double>(h->info.nnz_b) / h->info.n : 0.0;
+        if (avg_b >= 12.0 && cfg.l1_capacity <= 0) {
+            acc = kAccLP;
+            flat = false;
+            fast = true;
+        }
+    } else if (acc == kAccLP && !flat && cfg.l1_capacity <= 0) {
+        fast = true; // forced LP Thread-Sequential: same algorithm, fast kernel
+    }
+    h->num = plan_phase(acc, flat, kVarNumeric, h->info.k, h->size_hist.hist, h->info.max_row_size, cfg, fast, 0);
     if (h->d_num_list) {
         cudaFreeAsync(h->d_num_list, st);
         h->d_num_list = nullptr;
@@ -662,8 +750,11 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         bool sflat;
         device_choice(cfg.accumulator != SPG_ACC_AUTO, I.symbolic_choice, cfg, I.flops.avg_row_flops, variant,
                       domain, raw_bound, &sacc, &sflat);
-        const PhasePlan S =
-            plan_phase(sacc, sflat, variant, domain, apply ? htot->hist_cf : htot->hist_f, raw_bound, cfg);
+        // Auto: the order-free fast union with optimistic L1 sizing (kk_fast.cu)
+        const bool sfast = cfg.accumulator == SPG_ACC_AUTO && cfg.l1_capacity <= 0;
+        const PhasePlan S = plan_phase(sfast ? kAccLP : sacc, sfast ? true : sflat, variant, domain,
+                                       apply ? htot->hist_cf : htot->hist_f, raw_bound, cfg, sfast,
+                                       sfast ? std::max(cfg.collapse_divisor, 1) : 0);
         cuda_check(cudaMemsetAsync(h->d_rowptr, 0, sizeof(int64_t) * (int64_t{m} + 1), st), "memset");
         int32_t* d_list = nullptr;
         if (S.need_list) {
@@ -674,9 +765,15 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
                        "symbolic binning");
             cudaFreeAsync(fill, st);
         }
+        unsigned long long* d_retry_cnt = nullptr;
+        int32_t* d_retry = nullptr;
+        if (S.optimistic) {
+            d_retry_cnt = dalloc<unsigned long long>(1, st, "retry count");
+            d_retry = dalloc<int32_t>(std::max(m, 1), st, "retry rows");
+            cuda_check(cudaMemsetAsync(d_retry_cnt, 0, sizeof(unsigned long long), st), "memset");
+        }
         DevPool spool;
-        ensure_pool(spool, S, st);
-        for (const PhaseClass& pc : S.classes) {
+        auto sym_launch = [&](const PhaseClass& pc, const int32_t* list, int64_t nrows) {
             RowLaunch L{};
             L.a_rowptr = a->row_offsets;
             L.a_cols = a->col_indices;
@@ -686,17 +783,43 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             L.csize = d_csize;
             L.csi = d_csi;
             L.cs = d_cs;
-            L.list = S.need_list ? d_list + pc.off : nullptr;
-            L.nrows = S.need_list ? pc.count : m;
+            L.list = list;
+            L.nrows = nrows;
             L.sym_sizes = h->d_rowptr + 1;
             L.ctr = h->d_ctr;
             L.lay = pc.lay;
             L.wpb = pc.wpb;
             L.grid = pc.grid;
             L.l2 = pc.l2;
-            if (pc.l2)
-                L.pool = PoolDesc{spool.base, S.chunk_bytes, S.num_chunks, S.pool_mode, spool.states};
-            cuda_check(launch_row_kernel(L, S.acc, S.flat, S.variant, st), "symbolic kernel");
+            if (pc.l2) {
+                ensure_pool(spool, S.l2, st);
+                L.pool = PoolDesc{spool.base, S.l2.chunk_bytes, S.l2.num_chunks, S.l2.pool_mode, spool.states};
+                cuda_check(launch_row_kernel(L, S.fast ? kAccLP : S.acc, S.fast ? false : S.flat, S.variant, st),
+                           "symbolic L2 kernel");
+            } else if (pc.fast) {
+                cuda_check(launch_symbolic_fast(L, S.variant == kVarSymCompressed, d_retry_cnt, d_retry, st),
+                           "symbolic kernel");
+            } else {
+                cuda_check(launch_row_kernel(L, S.acc, S.flat, S.variant, st), "symbolic kernel");
+            }
+        };
+        for (const PhaseClass& pc : S.classes)
+            sym_launch(pc, S.need_list ? d_list + pc.off : nullptr, S.need_list ? pc.count : m);
+        if (S.optimistic) {
+            // rows whose optimistic L1 table overflowed: exact-size HBM tables
+            unsigned long long* hretry = reinterpret_cast<unsigned long long*>(hviews + 5);
+            cuda_check(cudaMemcpyAsync(hretry, d_retry_cnt, 8, cudaMemcpyDeviceToHost, st), "retry count");
+            cuda_check(cudaStreamSynchronize(st), "retry sync");
+            if (*hretry > 0) {
+                PhaseClass rc;
+                rc.l2 = true;
+                rc.lay = S.l2.lay;
+                rc.wpb = S.l2.wpb;
+                rc.grid = S.l2.grid;
+                sym_launch(rc, d_retry, static_cast<int64_t>(*hretry));
+            }
+            cudaFreeAsync(d_retry_cnt, st);
+            cudaFreeAsync(d_retry, st);
         }
         // ---- K2: scan ----
         cuda_check(scan_sizes_inplace(h->d_rowptr, m, d_stot, st), "scan");
@@ -769,8 +892,9 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
             cuda_check(cudaEventRecord(e0, st), "event");
         }
         cuda_check(cudaMemsetAsync(h->d_ctr, 0, sizeof(DevCounters), st), "memset");
-        ensure_pool(h->num_pool, h->num, st);
         const PhasePlan& P = h->num;
+        if (P.l2_class >= 0)
+            ensure_pool(h->num_pool, P.l2, st);
         for (const PhaseClass& pc : P.classes) {
             RowLaunch L{};
             L.a_rowptr = a->row_offsets;
@@ -789,9 +913,16 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
             L.wpb = pc.wpb;
             L.grid = pc.grid;
             L.l2 = pc.l2;
-            if (pc.l2)
-                L.pool = PoolDesc{h->num_pool.base, P.chunk_bytes, P.num_chunks, P.pool_mode, h->num_pool.states};
-            cuda_check(launch_row_kernel(L, P.acc, P.flat, kVarNumeric, st), "numeric kernel");
+            if (pc.l2) {
+                L.pool = PoolDesc{h->num_pool.base, P.l2.chunk_bytes, P.l2.num_chunks, P.l2.pool_mode,
+                                  h->num_pool.states};
+                cuda_check(launch_row_kernel(L, P.fast ? kAccLP : P.acc, P.fast ? false : P.flat, kVarNumeric, st),
+                           "numeric L2 kernel");
+            } else if (pc.fast) {
+                cuda_check(launch_numeric_fast(L, st), "numeric kernel");
+            } else {
+                cuda_check(launch_row_kernel(L, P.acc, P.flat, kVarNumeric, st), "numeric kernel");
+            }
         }
         if (I.config.sort_output)
             cuda_check(launch_sort_rows(I.m, h->d_rowptr, c_cols, c_vals, I.max_row_size, st), "sort_output");

@@ -1,0 +1,416 @@
+// Fast paths of the two row kernels (sm_100a), used by the default (Auto)
+// device plan.  Same semantics as the generic row_kernel in kk_kernels.cu —
+// the parity tests run both — with the per-product instruction count cut down:
+//
+// numeric_lp_seq_kernel   Thread-Sequential numeric Gustavson (engine.cpp:259-267)
+//     with a linear-probing L1 table in shared memory (keys[T], vals[T] by
+//     slot, slot_of[] by first-touch position) under a locality-preserving
+//     hash, so the entries of one B row (runs of consecutive columns on
+//     stencils) land in distinct banks.  New keys claim slots with a
+//     write-then-verify round instead of shared-memory CAS.  B rows of the
+//     next steps are prefetched into registers one batch ahead.  Positions
+//     are assigned in lane (= first-touch) order and values summed left to
+//     right with unfused mul/add, so C is bitwise the reference's output.
+//
+// symbolic_flat_kernel    Thread-Flat-Parallel structure union (engine.cpp:268-286
+//     with SymbolicSink :210-221) over the compressed graph (or raw columns).
+//     The union is order-independent, so duplicate keys inside a 32-product
+//     window are resolved with shared-memory CAS/OR instead of a warp fold,
+//     and the row size is the popcount of the table (no position bookkeeping).
+//     Tables are sized optimistically from the row bound; a row that overflows
+//     its table is re-queued to the HBM (L2) path, which is sized exactly.
+#include <cstdint>
+#include <cstdlib>
+
+#include "kk_device.cuh"
+#include "kk_internal.h"
+
+namespace kk {
+
+// ---------------------------------------------------------------------------
+// numeric: LP + Thread-Sequential
+// ---------------------------------------------------------------------------
+// Slot hash: Fibonacci (multiplicative) hash, linear probing.  (A
+// low-bit-preserving hash would keep B-row runs in distinct banks, but on
+// n = 160 stencils every run of a C row shares its low 5 bits — the same
+// pathology as the reference's key & mask hash, SURVEY §7 — and clusters.)
+constexpr uint32_t kProbeStep = 1;
+__device__ __forceinline__ uint32_t loc_hash(int32_t key, int shift)
+{
+    return hash_slot(key, shift);
+}
+
+// Claim empty slots for this step's new keys (distinct keys, first probe
+// already stopped at an empty slot `s`): write, re-read, losers move to the
+// next empty slot.  No shared-memory atomics.
+__device__ __forceinline__ uint32_t claim_slots(bool is_new, int32_t key, uint32_t s, int32_t* keys,
+                                                uint32_t tmask)
+{
+    bool pending = is_new;
+    for (;;) {
+        if (pending)
+            keys[s] = key;
+        __syncwarp();
+        if (pending && keys[s] == key)
+            pending = false;
+        if (!__any_sync(kFull, pending))
+            break;
+        if (pending)
+            do {
+                s = (s + kProbeStep) & tmask;
+            } while (keys[s] != kEmpty);
+        __syncwarp();
+    }
+    return s;
+}
+
+// one Thread-Sequential step: lanes hold distinct keys of one B row.
+// kCas: claim new slots with shared-memory CAS (else write-then-verify).
+template <bool kCas>
+__device__ __forceinline__ void num_step(bool valid, int32_t key, double v, int32_t* keys, double* vals,
+                                         int32_t* slot_of, uint32_t tmask, int shift, int32_t cap,
+                                         int32_t& cnt)
+{
+    uint32_t s = 0;
+    bool is_new = false;
+    if (valid) {
+        s = loc_hash(key, shift);
+        int32_t k = keys[s];
+        while (k != key && k != kEmpty) {
+            s = (s + kProbeStep) & tmask;
+            k = keys[s];
+        }
+        if (k == key) // running sum: ((first + v2) + v3) ...
+            vals[s] = __dadd_rn(vals[s], v);
+        else
+            is_new = true;
+    }
+    const uint32_t nm = __ballot_sync(kFull, is_new);
+    if (nm) {
+        if constexpr (kCas) {
+            if (is_new)
+                while (atomicCAS(&keys[s], kEmpty, key) != kEmpty)
+                    s = (s + kProbeStep) & tmask;
+        } else {
+            __syncwarp();
+            s = claim_slots(is_new, key, s, keys, tmask);
+        }
+        if (is_new) {
+            const int32_t pos = cnt + __popc(nm & lanemask_lt());
+            vals[s] = v;
+            if (pos < cap)
+                slot_of[pos] = static_cast<int32_t>(s);
+        }
+        cnt += __popc(nm);
+    }
+    __syncwarp();
+}
+
+// per-warp staging of one A chunk: the step scalars are read back with
+// broadcast LDS instead of 64-bit shuffles
+struct StepStage {
+    const int32_t* cp[32];
+    const double* vp[32];
+    double a[32];
+    int32_t len[32];
+};
+
+template <bool kCas>
+__global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    unsigned char* region = smem + (size_t)wib * L.lay.bytes;
+    double* vals = reinterpret_cast<double*>(region + L.lay.off_map);
+    int32_t* keys = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
+    int32_t* slot_of = reinterpret_cast<int32_t*>(region + L.lay.off_aux);
+    StepStage* stage = reinterpret_cast<StepStage*>(region + L.lay.off_pay);
+    const uint32_t tmask = static_cast<uint32_t>(L.lay.T - 1);
+    const int shift = L.lay.shift;
+    for (int t = lane; t < L.lay.T; t += 32)
+        keys[t] = kEmpty;
+    __syncwarp();
+
+    const int64_t nwarps = (int64_t)gridDim.x * L.wpb;
+    const int64_t* __restrict__ a_rowptr = L.a_rowptr;
+    const int32_t* __restrict__ a_cols = L.a_cols;
+    const double* __restrict__ a_vals = L.a_vals;
+    const int64_t* __restrict__ b_rowptr = L.b_rowptr;
+
+    for (int64_t r = (int64_t)blockIdx.x * L.wpb + wib; r < L.nrows; r += nwarps) {
+        const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        const int64_t cbase = __ldg(L.c_rowptr + i);
+        const int32_t cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
+        if (cap == 0)
+            continue;
+        const int64_t abeg = __ldg(a_rowptr + i), aend = __ldg(a_rowptr + i + 1);
+        int32_t cnt = 0;
+        for (int64_t p0 = abeg; p0 < aend; p0 += 32) {
+            const int na = static_cast<int>(aend - p0 < 32 ? aend - p0 : 32);
+            int32_t bl = 0;
+            if (lane < na) {
+                const int32_t j = __ldg(a_cols + p0 + lane);
+                const int64_t b0 = __ldg(b_rowptr + j);
+                bl = static_cast<int32_t>(__ldg(b_rowptr + j + 1) - b0);
+                stage->cp[lane] = L.b_cols + b0;
+                stage->vp[lane] = L.b_vals + b0;
+                stage->a[lane] = __ldg(a_vals + p0 + lane);
+                stage->len[lane] = bl;
+            }
+            const bool long_rows = __any_sync(kFull, bl > 32);
+            __syncwarp();
+            if (long_rows) {
+                // B rows longer than a warp: plain stepping
+                for (int q = 0; q < na; ++q) {
+                    const int32_t len = stage->len[q];
+                    const double a = stage->a[q];
+                    const int32_t* cp = stage->cp[q];
+                    const double* vp = stage->vp[q];
+                    for (int32_t t0 = 0; t0 < len; t0 += 32) {
+                        const bool valid = t0 + lane < len;
+                        int32_t key = 0;
+                        double v = 0.0;
+                        if (valid) {
+                            key = __ldg(cp + t0 + lane);
+                            v = __dmul_rn(a, __ldg(vp + t0 + lane));
+                        }
+                        num_step<kCas>(valid, key, v, keys, vals, slot_of, tmask, shift, cap, cnt);
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
+            // depth-2 register pipeline over the steps of the chunk
+            int32_t k0 = 0, k1 = 0;
+            double v0 = 0.0, v1 = 0.0;
+            if (lane < stage->len[0]) {
+                k0 = __ldg(stage->cp[0] + lane);
+                v0 = __ldg(stage->vp[0] + lane);
+            }
+            if (na > 1 && lane < stage->len[1]) {
+                k1 = __ldg(stage->cp[1] + lane);
+                v1 = __ldg(stage->vp[1] + lane);
+            }
+            for (int q = 0; q < na; ++q) {
+                int32_t k2 = 0;
+                double v2 = 0.0;
+                if (q + 2 < na && lane < stage->len[q + 2]) {
+                    k2 = __ldg(stage->cp[q + 2] + lane);
+                    v2 = __ldg(stage->vp[q + 2] + lane);
+                }
+                num_step<kCas>(lane < stage->len[q], k0, __dmul_rn(stage->a[q], v0), keys, vals, slot_of, tmask,
+                               shift, cap, cnt);
+                k0 = k1;
+                v0 = v1;
+                k1 = k2;
+                v1 = v2;
+            }
+            __syncwarp();
+        }
+        if (cnt != cap && lane == 0)
+            raise_error(L.ctr, cnt < cap ? kDevRowShort : kDevRowOverflow);
+        // flush in first-touch order and clear the table for the next row
+        const int32_t used = cnt < cap ? cnt : cap;
+        for (int32_t q = lane; q < used; q += 32) {
+            const int32_t s = slot_of[q];
+            L.c_cols[cbase + q] = keys[s];
+            L.c_vals[cbase + q] = vals[s];
+            keys[s] = kEmpty;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// symbolic: order-free union, LP table of {key, word} slots
+// ---------------------------------------------------------------------------
+template <bool kCompressed>
+__global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, unsigned long long* retry_count,
+                                                            int32_t* retry_list)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    unsigned char* region = smem + (size_t)wib * L.lay.bytes;
+    int32_t* keys = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
+    uint32_t* words = reinterpret_cast<uint32_t*>(region + L.lay.off_map);
+    const int T = L.lay.T;
+    const uint32_t tmask = static_cast<uint32_t>(T - 1);
+    const int pshift = L.lay.shift;
+    const int32_t cap = L.lay.S;
+    for (int t = lane; t < T; t += 32) {
+        keys[t] = kEmpty;
+        words[t] = 0u;
+    }
+    __syncwarp();
+
+    const int64_t nwarps = (int64_t)gridDim.x * L.wpb;
+    const int64_t* __restrict__ a_rowptr = L.a_rowptr;
+    const int32_t* __restrict__ a_cols = L.a_cols;
+    const int64_t* __restrict__ b_rowptr = L.b_rowptr;
+
+    for (int64_t r = (int64_t)blockIdx.x * L.wpb + wib; r < L.nrows; r += nwarps) {
+        const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        const int64_t abeg = __ldg(a_rowptr + i), aend = __ldg(a_rowptr + i + 1);
+        int32_t used = 0; // claimed slots (warp-uniform after each window)
+        bool overflow = false;
+        for (int64_t p0 = abeg; p0 < aend && !overflow; p0 += 32) {
+            const int na = static_cast<int>(aend - p0 < 32 ? aend - p0 : 32);
+            int64_t bb = 0;
+            int32_t bl = 0;
+            if (lane < na) {
+                const int32_t j = __ldg(a_cols + p0 + lane);
+                bb = __ldg(b_rowptr + j);
+                bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
+            }
+            int32_t incl = bl;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int32_t y = __shfl_up_sync(kFull, incl, off);
+                if (lane >= off)
+                    incl += y;
+            }
+            const int32_t excl = incl - bl;
+            const int32_t total = __shfl_sync(kFull, incl, 31);
+            for (int32_t w0 = 0; w0 < total; w0 += 32) {
+                const int32_t t = w0 + lane;
+                int seg = 0;
+#pragma unroll
+                for (int s = 16; s >= 1; s >>= 1) {
+                    const int32_t y = __shfl_sync(kFull, incl, seg + s - 1);
+                    if (y <= t)
+                        seg += s;
+                }
+                const int32_t e = __shfl_sync(kFull, excl, seg);
+                const int64_t base = __shfl_sync(kFull, bb, seg);
+                bool claimed = false;
+                if (t < total) {
+                    const int64_t q = base + (t - e);
+                    int32_t key;
+                    uint32_t word;
+                    if constexpr (kCompressed) {
+                        key = __ldg(L.csi + q);
+                        word = __ldg(L.cs + q);
+                    } else {
+                        key = __ldg(L.b_cols + q);
+                        word = 1u;
+                    }
+                    uint32_t s = loc_hash(key, pshift);
+                    for (int probes = 0; probes <= T; ++probes) {
+                        const int32_t k = keys[s];
+                        if (k == key)
+                            break;
+                        if (k == kEmpty) {
+                            const int32_t old = atomicCAS(&keys[s], kEmpty, key);
+                            if (old == kEmpty) {
+                                claimed = true;
+                                break;
+                            }
+                            if (old == key)
+                                break;
+                        }
+                        s = (s + kProbeStep) & tmask;
+                    }
+                    if constexpr (kCompressed)
+                        atomicOr(&words[s], word);
+                }
+                used += __popc(__ballot_sync(kFull, claimed));
+                if (used > cap) { // table too small for this row: hand it to the L2 path
+                    overflow = true;
+                    break;
+                }
+            }
+        }
+        __syncwarp();
+        int64_t size = 0;
+        for (int t = lane; t < T; t += 32) {
+            if (keys[t] != kEmpty) {
+                size += kCompressed ? __popc(words[t]) : 1;
+                keys[t] = kEmpty;
+                words[t] = 0u;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1)
+            size += __shfl_xor_sync(kFull, size, off);
+        if (lane == 0) {
+            if (overflow)
+                retry_list[atomicAdd(retry_count, 1ull)] = i;
+            else
+                L.sym_sizes[i] = size;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+cudaError_t launch_numeric_fast(const RowLaunch& L, cudaStream_t st)
+{
+    if (L.nrows <= 0 || L.grid <= 0)
+        return cudaSuccess;
+    const size_t smem = (size_t)L.wpb * L.lay.bytes;
+    const bool cas = getenv("KK_NUM_VERIFY") == nullptr; // CAS claims by default (measured faster)
+    const void* fn = cas ? reinterpret_cast<const void*>(&numeric_lp_seq_kernel<true>)
+                         : reinterpret_cast<const void*>(&numeric_lp_seq_kernel<false>);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return e;
+    }
+    if (cas)
+        numeric_lp_seq_kernel<true><<<L.grid, L.wpb * 32, smem, st>>>(L);
+    else
+        numeric_lp_seq_kernel<false><<<L.grid, L.wpb * 32, smem, st>>>(L);
+    count_launch();
+    return cudaGetLastError();
+}
+
+int numeric_fast_blocks_per_sm(int wpb, size_t smem)
+{
+    const void* fn = reinterpret_cast<const void*>(&numeric_lp_seq_kernel<false>);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(&numeric_lp_seq_kernel<true>),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, wpb * 32, smem) != cudaSuccess)
+        return 1;
+    return b > 0 ? b : 1;
+}
+
+cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, unsigned long long* retry_count,
+                                 int32_t* retry_list, cudaStream_t st)
+{
+    if (L.nrows <= 0 || L.grid <= 0)
+        return cudaSuccess;
+    const size_t smem = (size_t)L.wpb * L.lay.bytes;
+    const void* fn = compressed ? reinterpret_cast<const void*>(&symbolic_flat_kernel<true>)
+                                : reinterpret_cast<const void*>(&symbolic_flat_kernel<false>);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return e;
+    }
+    if (compressed)
+        symbolic_flat_kernel<true><<<L.grid, L.wpb * 32, smem, st>>>(L, retry_count, retry_list);
+    else
+        symbolic_flat_kernel<false><<<L.grid, L.wpb * 32, smem, st>>>(L, retry_count, retry_list);
+    count_launch();
+    return cudaGetLastError();
+}
+
+int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem)
+{
+    const void* fn = compressed ? reinterpret_cast<const void*>(&symbolic_flat_kernel<true>)
+                                : reinterpret_cast<const void*>(&symbolic_flat_kernel<false>);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, wpb * 32, smem) != cudaSuccess)
+        return 1;
+    return b > 0 ? b : 1;
+}
+
+} // namespace kk

@@ -97,6 +97,13 @@ cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, do
 cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals* tot,
                                    cudaStream_t st);
 
+// fast paths (kk_fast.cu)
+cudaError_t launch_numeric_fast(const RowLaunch& L, cudaStream_t st);
+int numeric_fast_blocks_per_sm(int wpb, size_t smem);
+cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, unsigned long long* retry_count,
+                                 int32_t* retry_list, cudaStream_t st);
+int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem);
+
 void count_launch(int n = 1);
 int sm_count();
 
