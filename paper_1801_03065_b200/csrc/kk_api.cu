@@ -244,7 +244,7 @@ TabLayout make_layout_fast(int variant, int32_t S, double occupancy)
         L.off_ids = static_cast<uint32_t>(8ull * L.T);          // keys  [T] int32
         L.off_aux = static_cast<uint32_t>(12ull * L.T);         // slot_of [S]
         L.off_pay = static_cast<uint32_t>(align_up(12ull * L.T + 4ull * L.S, 16)); // step stage
-        L.bytes = L.off_pay + 896;
+        L.bytes = L.off_pay + 768; // StepStage
     } else {
         L.off_ids = 0;                                          // keys  [T]
         L.off_map = static_cast<uint32_t>(4ull * L.T);          // words [T]

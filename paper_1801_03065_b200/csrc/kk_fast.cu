@@ -107,12 +107,11 @@ __device__ __forceinline__ void num_step(bool valid, int32_t key, double v, int3
 }
 
 // per-warp staging of one A chunk: the step scalars are read back with
-// broadcast LDS instead of 64-bit shuffles
+// broadcast LDS (one 16-byte {B row offset, length} read for the prefetch of
+// step q+2, one 8-byte read of A(i,j) for step q)
 struct StepStage {
-    const int32_t* cp[32];
-    const double* vp[32];
+    longlong2 row[32]; // x = B row offset, y = B row length
     double a[32];
-    int32_t len[32];
 };
 
 template <bool kCas>
@@ -153,27 +152,26 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
                 const int32_t j = __ldg(a_cols + p0 + lane);
                 const int64_t b0 = __ldg(b_rowptr + j);
                 bl = static_cast<int32_t>(__ldg(b_rowptr + j + 1) - b0);
-                stage->cp[lane] = L.b_cols + b0;
-                stage->vp[lane] = L.b_vals + b0;
+                stage->row[lane] = make_longlong2(b0, bl);
                 stage->a[lane] = __ldg(a_vals + p0 + lane);
-                stage->len[lane] = bl;
+            } else {
+                stage->row[lane] = make_longlong2(0, 0);
             }
             const bool long_rows = __any_sync(kFull, bl > 32);
             __syncwarp();
             if (long_rows) {
                 // B rows longer than a warp: plain stepping
                 for (int q = 0; q < na; ++q) {
-                    const int32_t len = stage->len[q];
+                    const longlong2 rq = stage->row[q];
+                    const int32_t len = static_cast<int32_t>(rq.y);
                     const double a = stage->a[q];
-                    const int32_t* cp = stage->cp[q];
-                    const double* vp = stage->vp[q];
                     for (int32_t t0 = 0; t0 < len; t0 += 32) {
                         const bool valid = t0 + lane < len;
                         int32_t key = 0;
                         double v = 0.0;
                         if (valid) {
-                            key = __ldg(cp + t0 + lane);
-                            v = __dmul_rn(a, __ldg(vp + t0 + lane));
+                            key = __ldg(L.b_cols + rq.x + t0 + lane);
+                            v = __dmul_rn(a, __ldg(L.b_vals + rq.x + t0 + lane));
                         }
                         num_step<kCas>(valid, key, v, keys, vals, slot_of, tmask, shift, cap, cnt);
                     }
@@ -181,30 +179,43 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
                 __syncwarp();
                 continue;
             }
-            // depth-2 register pipeline over the steps of the chunk
-            int32_t k0 = 0, k1 = 0;
+            // depth-2 register pipeline over the steps of the chunk (rows of
+            // the stage past na have length 0)
+            int32_t k0 = 0, k1 = 0, len0, len1;
             double v0 = 0.0, v1 = 0.0;
-            if (lane < stage->len[0]) {
-                k0 = __ldg(stage->cp[0] + lane);
-                v0 = __ldg(stage->vp[0] + lane);
-            }
-            if (na > 1 && lane < stage->len[1]) {
-                k1 = __ldg(stage->cp[1] + lane);
-                v1 = __ldg(stage->vp[1] + lane);
+            {
+                const longlong2 r0 = stage->row[0];
+                const longlong2 r1 = stage->row[1];
+                len0 = static_cast<int32_t>(r0.y);
+                len1 = static_cast<int32_t>(r1.y);
+                if (lane < len0) {
+                    k0 = __ldg(L.b_cols + r0.x + lane);
+                    v0 = __ldg(L.b_vals + r0.x + lane);
+                }
+                if (lane < len1) {
+                    k1 = __ldg(L.b_cols + r1.x + lane);
+                    v1 = __ldg(L.b_vals + r1.x + lane);
+                }
             }
             for (int q = 0; q < na; ++q) {
-                int32_t k2 = 0;
+                int32_t k2 = 0, len2 = 0;
                 double v2 = 0.0;
-                if (q + 2 < na && lane < stage->len[q + 2]) {
-                    k2 = __ldg(stage->cp[q + 2] + lane);
-                    v2 = __ldg(stage->vp[q + 2] + lane);
+                if (q + 2 < 32) {
+                    const longlong2 r2 = stage->row[q + 2];
+                    len2 = static_cast<int32_t>(r2.y);
+                    if (lane < len2) {
+                        k2 = __ldg(L.b_cols + r2.x + lane);
+                        v2 = __ldg(L.b_vals + r2.x + lane);
+                    }
                 }
-                num_step<kCas>(lane < stage->len[q], k0, __dmul_rn(stage->a[q], v0), keys, vals, slot_of, tmask,
-                               shift, cap, cnt);
+                num_step<kCas>(lane < len0, k0, __dmul_rn(stage->a[q], v0), keys, vals, slot_of, tmask, shift,
+                               cap, cnt);
                 k0 = k1;
                 v0 = v1;
+                len0 = len1;
                 k1 = k2;
                 v1 = v2;
+                len1 = len2;
             }
             __syncwarp();
         }

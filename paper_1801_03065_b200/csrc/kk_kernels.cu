@@ -201,7 +201,19 @@ __global__ void __launch_bounds__(256) flops_kernel(int32_t m, const int64_t* __
         int64_t f = 0, cf = 0;
         if (i < m) {
             const int64_t beg = __ldg(a_rowptr + i), end = __ldg(a_rowptr + i + 1);
-            for (int64_t p = beg + glane; p < end; p += G) {
+            int64_t p = beg + glane;
+            for (; p + 3 * G < end; p += 4 * G) {
+                int32_t j[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    j[u] = __ldg(a_cols + p + u * G);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    f += __ldg(b_rowptr + j[u] + 1) - __ldg(b_rowptr + j[u]);
+                    cf += __ldg(csize + j[u]);
+                }
+            }
+            for (; p < end; p += G) {
                 const int32_t j = __ldg(a_cols + p);
                 f += __ldg(b_rowptr + j + 1) - __ldg(b_rowptr + j);
                 cf += __ldg(csize + j);
@@ -743,8 +755,10 @@ cudaError_t launch_flops(int32_t m, double avg_len, const int64_t* a_rowptr, con
 {
     if (m <= 0)
         return cudaSuccess;
+    // lanes per row: ~4 entries per lane so every lane has several independent
+    // gathers in flight (the kernel is latency-bound, not bandwidth-bound)
     int g = 1;
-    while (g < 32 && g < avg_len)
+    while (g < 32 && 4 * g < avg_len)
         g <<= 1;
     const int rows_per_block = 256 / g;
     const int blocks = (int)std::min<int64_t>((m + rows_per_block - 1) / rows_per_block, (int64_t)sm_count() * 8);
