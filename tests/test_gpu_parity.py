@@ -290,3 +290,30 @@ def test_c1_full_size_vs_oracle(kk, oracle):
     _, c = run(kk, a, a)
     assert c.nnz() == 12_980_004
     assert_parity(oracle, a, a, c)
+
+
+def test_c4_rmat_row_sampled(kk, oracle):
+    """Config 4's R-MAT at scale 17 (skewed rows, L2 pool path): row-sampled
+    parity (every 32nd row + the 128 heaviest), bitwise raw order.  Rows of C
+    are independent, so a row sample of A times full B is exact."""
+    from paper_1801_03065_b200 import generators as G
+    a = G.rmat(17, 16, 1)
+    res = kk.multiply(a, a)
+    h = res.handle
+    assert h.symbolic_stats.pool_allocations + res.numeric_stats.pool_allocations > 0
+    ro = h.c_row_offsets
+    sizes = np.diff(ro)
+    rows = np.unique(np.concatenate([np.arange(0, a.num_rows, 32), np.argsort(sizes)[-128:]]))
+    lo, hi = a.row_offsets[rows], a.row_offsets[rows + 1]
+    sro = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(hi - lo, out=sro[1:])
+    idx = np.concatenate([np.arange(l, e) for l, e in zip(lo, hi)])
+    asamp = kk.CsrMatrix(len(rows), a.num_cols, sro, a.col_indices[idx], a.values[idx], True)
+    oro, ocols, ovals = oracle.multiply(asamp, a)
+    assert np.array_equal(np.diff(oro), sizes[rows])
+    gcols = res.c.col_indices.cpu().numpy()
+    gvals = res.c.values.cpu().numpy()
+    for q, i in enumerate(rows):
+        gs, ge = int(ro[i]), int(ro[i + 1])
+        assert np.array_equal(gcols[gs:ge], ocols[oro[q]:oro[q + 1]])
+        assert np.array_equal(gvals[gs:ge].view(np.int64), ovals[oro[q]:oro[q + 1]].view(np.int64))
