@@ -216,18 +216,11 @@ def main():
     m = a_host.num_rows
 
     # ---- flop-balanced row partition, not timed ----
+    from paper_1801_03065_b200 import shard
     lo, hi = 0, m
     if world > 1:
-        # per-row flops (sum of the referenced B row sizes) for the cut points
-        prf = torch.from_numpy(np.diff(a_host.row_offsets)).to(dev)
-        brs = (B.row_offsets[1:] - B.row_offsets[:-1])
-        rows_of = torch.repeat_interleave(torch.arange(m, device=dev), prf)
-        f = torch.zeros(m, dtype=torch.int64, device=dev).index_add_(0, rows_of, brs[A.col_indices.long()])
-        cum = torch.cumsum(f, 0)
-        total = int(cum[-1].item())
-        cuts = [0] + [int(torch.searchsorted(cum, total * g // world, right=False).item()) for g in range(1, world)] + [m]
+        cuts = shard.flop_cut_points(torch.cumsum(kk.row_flops(A, B), 0), world)
         lo, hi = cuts[rank], cuts[rank + 1]
-        del rows_of, f, cum, prf
     A_shard = A.row_block(lo, hi)
 
     # ---- warm-up and one reference multiply for counts ----
@@ -239,8 +232,9 @@ def main():
     vals = torch.empty(max(nnz_c_local, 1), dtype=torch.float64, device=dev)
 
     def bcast_b():
+        # B broadcast over NCCL from rank 0 every step (the "with broadcast" timing)
         if world > 1 and args.broadcast:
-            for t in (B.row_offsets, B.col_indices, B.values):
+            for t in (B.row_offsets, B.col_indices, B.values):  # in place: ranks > 0 compute on it
                 dist.broadcast(t, src=0)
 
     def step_symnum():

@@ -206,6 +206,11 @@ void spg_handle_destroy(spg_handle_t h);
 int spg_sort_rows(int32_t m, const int64_t* d_row_offsets, int32_t* d_cols, double* d_vals,
                   void* stream);
 
+/* Per-row multiplication counts (flops_stats per_row_flops, csr_matrix.cpp:136-154)
+ * into device memory d_out[a->num_rows]; stream-ordered.  Used for the
+ * flop-balanced row partition of the multi-GPU path. */
+int spg_row_flops(const spg_csr* a, const spg_csr* b, int64_t* d_out, void* stream);
+
 /* Number of kernels this library launched since load (evidence counter). */
 int64_t spg_kernel_launch_count(void);
 

@@ -158,6 +158,7 @@ EXPORTED_SYMBOLS = (
     "spg_symbolic", "spg_numeric", "spg_handle_info_get", "spg_handle_copy_row_offsets",
     "spg_handle_copy_per_row_flops", "spg_handle_copy_row_offsets_device", "spg_handle_set_numeric", "spg_handle_import",
     "spg_handle_check", "spg_handle_destroy", "spg_sort_rows", "spg_kernel_launch_count",
+    "spg_row_flops",
 )
 
 _lib_handle = None
@@ -177,7 +178,7 @@ def lib() -> C.CDLL:
         for name in ("spg_config_init", "spg_resolve_config", "spg_flat_position", "spg_symbolic",
                      "spg_numeric", "spg_handle_info_get", "spg_handle_copy_row_offsets",
                      "spg_handle_copy_per_row_flops", "spg_handle_copy_row_offsets_device", "spg_handle_set_numeric",
-                     "spg_handle_import", "spg_handle_check", "spg_sort_rows"):
+                     "spg_handle_import", "spg_handle_check", "spg_sort_rows", "spg_row_flops"):
             getattr(L, name).restype = C.c_int
         L.spg_symbolic.argtypes = [C.POINTER(_Csr), C.POINTER(_Csr), C.POINTER(_Config),
                                    C.POINTER(C.c_void_p), C.c_void_p]
@@ -196,6 +197,7 @@ def lib() -> C.CDLL:
         L.spg_flat_position.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_int32),
                                         C.POINTER(C.c_int64)]
         L.spg_sort_rows.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.spg_row_flops.argtypes = [C.POINTER(_Csr), C.POINTER(_Csr), C.c_void_p, C.c_void_p]
         _lib_handle = L
     return _lib_handle
 
@@ -557,6 +559,15 @@ def import_handle(m: int, n: int, k: int, nnz_a: int, nnz_b: int, c_row_offsets:
     ptr = C.c_void_p()
     _check(lib().spg_handle_import(C.byref(d), C.byref(ptr), _stream_ptr(None)))
     return SpgemmHandle(ptr.value)
+
+
+def row_flops(a, b, stream=None):
+    """Per-row multiplication counts on the device (torch.int64 [m])."""
+    import torch
+    da, db = _dev(a), _dev(b)
+    out = torch.empty(max(da.num_rows, 1), dtype=torch.int64, device=da.row_offsets.device)
+    _check(lib().spg_row_flops(C.byref(da._c()), C.byref(db._c()), out.data_ptr(), _stream_ptr(stream)))
+    return out[:da.num_rows]
 
 
 def sort_rows(c: DeviceCsr, stream=None) -> DeviceCsr:

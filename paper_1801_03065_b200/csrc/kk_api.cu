@@ -1079,6 +1079,22 @@ void spg_handle_destroy(spg_handle_t h)
     }
 }
 
+int spg_row_flops(const spg_csr* a, const spg_csr* b, int64_t* d_out, void* stream)
+{
+    return guarded([&] {
+        validate_csr(a, "row_flops: A", false);
+        validate_csr(b, "row_flops: B", false);
+        if (a->num_cols != b->num_rows)
+            fail(SPG_ERR_CONTRACT, "flops_stats: inner dimensions do not match");
+        if (!d_out && a->num_rows > 0)
+            fail(SPG_ERR_CONTRACT, "row_flops: null output");
+        require_device();
+        cuda_check(launch_row_flops(a->num_rows, a->row_offsets, a->col_indices, b->row_offsets, d_out,
+                                    static_cast<cudaStream_t>(stream)),
+                   "row flops");
+    });
+}
+
 int spg_sort_rows(int32_t m, const int64_t* d_row_offsets, int32_t* d_cols, double* d_vals, void* stream)
 {
     return guarded([&] {

@@ -94,6 +94,8 @@ int row_kernel_max_blocks_per_sm(int acc, bool flat, int variant, bool l2, int w
 cudaError_t scan_sizes_inplace(int64_t* rowptr, int64_t m, ScanTotals* tot, cudaStream_t st);
 cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, double* vals,
                              int64_t max_row, cudaStream_t st);
+cudaError_t launch_row_flops(int32_t m, const int64_t* a_rowptr, const int32_t* a_cols,
+                             const int64_t* b_rowptr, int64_t* out, cudaStream_t st);
 cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals* tot,
                                    cudaStream_t st);
 

@@ -616,6 +616,40 @@ cudaError_t scan_sizes_inplace(int64_t* rowptr, int64_t m, ScanTotals* tot, cuda
     return inclusive_scan(rowptr + 1, m, tot, st);
 }
 
+// per-row flops only (K1 without compression): the flop-balanced row
+// partition of the multi-GPU path.  Warp per row.
+__global__ void __launch_bounds__(256) row_flops_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,
+                                                        const int32_t* __restrict__ a_cols,
+                                                        const int64_t* __restrict__ b_rowptr,
+                                                        int64_t* __restrict__ out)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
+        int64_t f = 0;
+        for (int64_t p = __ldg(a_rowptr + i) + lane; p < __ldg(a_rowptr + i + 1); p += 32) {
+            const int32_t j = __ldg(a_cols + p);
+            f += __ldg(b_rowptr + j + 1) - __ldg(b_rowptr + j);
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1)
+            f += __shfl_xor_sync(kFull, f, off);
+        if (lane == 0)
+            out[i] = f;
+    }
+}
+
+cudaError_t launch_row_flops(int32_t m, const int64_t* a_rowptr, const int32_t* a_cols, const int64_t* b_rowptr,
+                             int64_t* out, cudaStream_t st)
+{
+    if (m <= 0)
+        return cudaSuccess;
+    const int blocks = (int)std::min<int64_t>((m + 7) / 8, (int64_t)sm_count() * 8);
+    row_flops_kernel<<<blocks, 256, 0, st>>>(m, a_rowptr, a_cols, b_rowptr, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
 __global__ void row_hist_kernel(int32_t m, const int64_t* __restrict__ rowptr, ScanTotals* tot)
 {
     __shared__ unsigned long long sh_hist[64];

@@ -317,3 +317,36 @@ def test_c4_rmat_row_sampled(kk, oracle):
         gs, ge = int(ro[i]), int(ro[i + 1])
         assert np.array_equal(gcols[gs:ge], ocols[oro[q]:oro[q + 1]])
         assert np.array_equal(gvals[gs:ge].view(np.int64), ovals[oro[q]:oro[q + 1]].view(np.int64))
+
+
+def test_row_flops_kernel(kk, oracle):
+    from paper_1801_03065_b200 import generators as G
+    a = G.rmat(12, 16, 1)
+    per, _, _ = oracle.flops_stats(a, a)
+    assert np.array_equal(kk.row_flops(a.to_device(), a.to_device()).cpu().numpy(), per)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_flop_balanced_shards_reassemble(kk, oracle, world):
+    """Multi-GPU partition emulated shard by shard on one GPU:
+    GPU per-row flops -> cut points -> row-block multiplies; the blocks with
+    their all-gathered base offsets reassemble C bit for bit."""
+    import torch
+    from paper_1801_03065_b200 import generators as G, shard
+    a = G.laplace3d(14)
+    da = a.to_device()
+    cuts = shard.flop_cut_points(torch.cumsum(kk.row_flops(da, da), 0), world)
+    ro, cols, vals = oracle.multiply(a, a)
+    nnzs, flops = [], []
+    for r in range(world):
+        res = kk.multiply(da.row_block(cuts[r], cuts[r + 1]), da)
+        c = res.c.to_host()
+        nnzs.append(c.nnz())
+        flops.append(res.handle.flops.total_flops)
+        lo, hi = cuts[r], cuts[r + 1]
+        assert np.array_equal(c.row_offsets + ro[lo], ro[lo:hi + 1])
+        assert np.array_equal(c.col_indices, cols[ro[lo]:ro[hi]])
+        assert np.array_equal(c.values.view(np.int64), vals[ro[lo]:ro[hi]].view(np.int64))
+    offs = shard.block_offsets(nnzs)
+    assert offs == [int(ro[c]) for c in cuts]
+    assert max(flops) - min(flops) <= 729
