@@ -366,7 +366,7 @@ def main():
         "numeric_only": {"value": value_num, "unit": UNIT, "ms_per_step": ms_num},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": load_traffic(f"c{args.config}_numeric"),
-                     "kernel": "row_kernel (numeric)", "peak_kind": peak_kind,
+                     "kernel": "numeric_lp_seq_kernel (numeric phase)", "peak_kind": peak_kind,
                      "algorithmic_bytes": bytes_num,
                      "model": "16(m+1)+28nnzA+12flops+12nnzC (SURVEY §8d)"},
         "cpu_baseline": cpu,

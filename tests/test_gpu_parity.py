@@ -349,4 +349,4 @@ def test_flop_balanced_shards_reassemble(kk, oracle, world):
         assert np.array_equal(c.values.view(np.int64), vals[ro[lo]:ro[hi]].view(np.int64))
     offs = shard.block_offsets(nnzs)
     assert offs == [int(ro[c]) for c in cuts]
-    assert max(flops) - min(flops) <= 729
+    assert max(flops) - min(flops) <= 2 * 729  # lower_bound cuts: within two rows
