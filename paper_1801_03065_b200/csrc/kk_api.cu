@@ -364,7 +364,8 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
             if (!fast)
                 per_sm = row_kernel_max_blocks_per_sm(acc, flat, variant, false, pc.wpb, smem);
             else if (variant == kVarNumeric)
-                per_sm = numeric_fast_blocks_per_sm(pc.wpb, smem);
+                per_sm = flat ? numeric_flat_fast_blocks_per_sm(pc.wpb, smem)
+                              : numeric_fast_blocks_per_sm(pc.wpb, smem);
             else
                 per_sm = symbolic_fast_blocks_per_sm(variant == kVarSymCompressed, pc.wpb, smem);
             const int64_t want = (pc.count + pc.wpb - 1) / pc.wpb;
@@ -515,13 +516,13 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
         // Thread-Sequential (one B row per step, warp lanes over its entries)
         // when rows fill a good part of the warp, Thread-Flat otherwise.
         const double avg_b = h->info.n > 0 ? static_cast<double>(h->info.nnz_b) / h->info.n : 0.0;
-        if (avg_b >= 12.0 && cfg.l1_capacity <= 0) {
+        if (cfg.l1_capacity <= 0) {
             acc = kAccLP;
-            flat = false;
+            flat = avg_b < 12.0;
             fast = true;
         }
-    } else if (acc == kAccLP && !flat && cfg.l1_capacity <= 0) {
-        fast = true; // forced LP Thread-Sequential: same algorithm, fast kernel
+    } else if (acc == kAccLP && cfg.l1_capacity <= 0) {
+        fast = true; // forced LP: same algorithms, fast kernels
     }
     h->num = plan_phase(acc, flat, kVarNumeric, h->info.k, h->size_hist.hist, h->info.max_row_size, cfg, fast, 0);
     if (h->d_num_list) {
@@ -919,7 +920,7 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
                 cuda_check(launch_row_kernel(L, P.fast ? kAccLP : P.acc, P.fast ? false : P.flat, kVarNumeric, st),
                            "numeric L2 kernel");
             } else if (pc.fast) {
-                cuda_check(launch_numeric_fast(L, st), "numeric kernel");
+                cuda_check(P.flat ? launch_numeric_flat_fast(L, st) : launch_numeric_fast(L, st), "numeric kernel");
             } else {
                 cuda_check(launch_row_kernel(L, P.acc, P.flat, kVarNumeric, st), "numeric kernel");
             }

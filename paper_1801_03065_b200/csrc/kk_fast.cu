@@ -234,6 +234,173 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
 }
 
 // ---------------------------------------------------------------------------
+// numeric: LP + Thread-Flat-Parallel (short B rows)
+// ---------------------------------------------------------------------------
+// One 32-product window of the row's flattened multiplications (engine.cpp:
+// 268-286).  Duplicate keys inside the window come from different A entries:
+// __match_any_sync groups them, the lowest lane (first touch) probes/claims,
+// and folds the group's products in lane (= product) order onto the running
+// sum, so values stay the reference's left-to-right sums.
+__device__ __forceinline__ void num_window(bool valid, int32_t key, double v, int32_t* keys, double* vals,
+                                           int32_t* slot_of, uint32_t tmask, int shift, int32_t cap,
+                                           int32_t& cnt, int lane)
+{
+    const uint32_t grp = __match_any_sync(kFull, valid ? key : (-1 - lane));
+    const bool leader = valid && (__ffs(grp) - 1) == lane;
+    uint32_t s = 0;
+    bool is_new = false;
+    double acc = v;
+    if (leader) {
+        s = loc_hash(key, shift);
+        int32_t k = keys[s];
+        while (k != key && k != kEmpty) {
+            s = (s + kProbeStep) & tmask;
+            k = keys[s];
+        }
+        if (k == key)
+            acc = __dadd_rn(vals[s], v);
+        else
+            is_new = true;
+    }
+    const uint32_t nm = __ballot_sync(kFull, is_new);
+    if (nm) {
+        if (is_new) {
+            while (atomicCAS(&keys[s], kEmpty, key) != kEmpty)
+                s = (s + kProbeStep) & tmask;
+            const int32_t pos = cnt + __popc(nm & lanemask_lt());
+            if (pos < cap)
+                slot_of[pos] = static_cast<int32_t>(s);
+        }
+        cnt += __popc(nm);
+    }
+    uint32_t rest = leader ? (grp & (grp - 1)) : 0u;
+    const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(rest)));
+    for (int r = 0; r < rounds; ++r) {
+        const int src = rest ? __ffs(rest) - 1 : lane;
+        const double x = __shfl_sync(kFull, v, src);
+        if (rest) {
+            acc = __dadd_rn(acc, x);
+            rest &= rest - 1;
+        }
+    }
+    if (leader)
+        vals[s] = acc;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    unsigned char* region = smem + (size_t)wib * L.lay.bytes;
+    double* vals = reinterpret_cast<double*>(region + L.lay.off_map);
+    int32_t* keys = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
+    int32_t* slot_of = reinterpret_cast<int32_t*>(region + L.lay.off_aux);
+    const uint32_t tmask = static_cast<uint32_t>(L.lay.T - 1);
+    const int shift = L.lay.shift;
+    for (int t = lane; t < L.lay.T; t += 32)
+        keys[t] = kEmpty;
+    __syncwarp();
+
+    const int64_t nwarps = (int64_t)gridDim.x * L.wpb;
+    const int64_t* __restrict__ a_rowptr = L.a_rowptr;
+    const int64_t* __restrict__ b_rowptr = L.b_rowptr;
+
+    for (int64_t r = (int64_t)blockIdx.x * L.wpb + wib; r < L.nrows; r += nwarps) {
+        const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        const int64_t cbase = __ldg(L.c_rowptr + i);
+        const int32_t cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
+        if (cap == 0)
+            continue;
+        const int64_t abeg = __ldg(a_rowptr + i), aend = __ldg(a_rowptr + i + 1);
+        int32_t cnt = 0;
+        for (int64_t p0 = abeg; p0 < aend; p0 += 32) {
+            const int na = static_cast<int>(aend - p0 < 32 ? aend - p0 : 32);
+            int64_t bb = 0;
+            int32_t bl = 0;
+            double av = 0.0;
+            if (lane < na) {
+                const int32_t j = __ldg(L.a_cols + p0 + lane);
+                av = __ldg(L.a_vals + p0 + lane);
+                bb = __ldg(b_rowptr + j);
+                bl = static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
+            }
+            // flattened prefix of this chunk's B-row lengths (32-bit: one
+            // chunk of a flat-scheme row never holds 2^31 products)
+            int32_t incl = bl;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int32_t y = __shfl_up_sync(kFull, incl, off);
+                if (lane >= off)
+                    incl += y;
+            }
+            const int32_t excl = incl - bl;
+            const int32_t total = __shfl_sync(kFull, incl, 31);
+            for (int32_t w0 = 0; w0 < total; w0 += 32) {
+                const int32_t t = w0 + lane;
+                int seg = 0; // upper_bound(prefix, t) - 1 (flat_position, engine.cpp:360-365)
+#pragma unroll
+                for (int s = 16; s >= 1; s >>= 1) {
+                    const int32_t y = __shfl_sync(kFull, incl, seg + s - 1);
+                    if (y <= t)
+                        seg += s;
+                }
+                const int32_t e = __shfl_sync(kFull, excl, seg);
+                const int64_t base = __shfl_sync(kFull, bb, seg);
+                const double a = __shfl_sync(kFull, av, seg);
+                const bool valid = t < total;
+                int32_t key = 0;
+                double v = 0.0;
+                if (valid) {
+                    const int64_t q = base + (t - e);
+                    key = __ldg(L.b_cols + q);
+                    v = __dmul_rn(a, __ldg(L.b_vals + q));
+                }
+                num_window(valid, key, v, keys, vals, slot_of, tmask, shift, cap, cnt, lane);
+            }
+        }
+        if (cnt != cap && lane == 0)
+            raise_error(L.ctr, cnt < cap ? kDevRowShort : kDevRowOverflow);
+        const int32_t used = cnt < cap ? cnt : cap;
+        for (int32_t q = lane; q < used; q += 32) {
+            const int32_t s = slot_of[q];
+            L.c_cols[cbase + q] = keys[s];
+            L.c_vals[cbase + q] = vals[s];
+            keys[s] = kEmpty;
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_numeric_flat_fast(const RowLaunch& L, cudaStream_t st)
+{
+    if (L.nrows <= 0 || L.grid <= 0)
+        return cudaSuccess;
+    const size_t smem = (size_t)L.wpb * L.lay.bytes;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&numeric_lp_flat_kernel),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return e;
+    }
+    numeric_lp_flat_kernel<<<L.grid, L.wpb * 32, smem, st>>>(L);
+    count_launch();
+    return cudaGetLastError();
+}
+
+int numeric_flat_fast_blocks_per_sm(int wpb, size_t smem)
+{
+    const void* fn = reinterpret_cast<const void*>(&numeric_lp_flat_kernel);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, wpb * 32, smem) != cudaSuccess)
+        return 1;
+    return b > 0 ? b : 1;
+}
+
+// ---------------------------------------------------------------------------
 // symbolic: order-free union, LP table of {key, word} slots
 // ---------------------------------------------------------------------------
 template <bool kCompressed>

@@ -102,6 +102,8 @@ cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals*
 // fast paths (kk_fast.cu)
 cudaError_t launch_numeric_fast(const RowLaunch& L, cudaStream_t st);
 int numeric_fast_blocks_per_sm(int wpb, size_t smem);
+cudaError_t launch_numeric_flat_fast(const RowLaunch& L, cudaStream_t st);
+int numeric_flat_fast_blocks_per_sm(int wpb, size_t smem);
 cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, unsigned long long* retry_count,
                                  int32_t* retry_list, cudaStream_t st);
 int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem);
