@@ -44,6 +44,17 @@ __device__ __forceinline__ int bucket_of(unsigned long long x)
     return x == 0 ? 0 : min(65 - __clzll(x - 1), 63);
 }
 
+// Warp-aggregated histogram increment (all 32 lanes, converged): one shared
+// atomic per distinct bucket instead of one per lane (rows of a stencil all
+// fall in the same bucket, which serialised the per-lane atomics).  b < 0
+// contributes nothing.
+__device__ __forceinline__ void warp_hist_add(unsigned long long* sh, int b, int lane)
+{
+    const uint32_t grp = __match_any_sync(kFull, b);
+    if (b >= 0 && (__ffs(grp) - 1) == lane)
+        atomicAdd(&sh[b], static_cast<unsigned long long>(__popc(grp)));
+}
+
 // OR of v over the lanes of `grp` (a __match_any_sync group), every lane
 // receiving its own group's result.  Group membership is arbitrary, so the
 // members are visited one by one (rounds = largest group).
@@ -70,15 +81,76 @@ __device__ __forceinline__ uint32_t group_or(uint32_t grp, uint32_t v, int lane)
 // for sorted rows; unsorted long rows use an order-insensitive merge (the
 // compressed graph only feeds the order-independent bit-OR union).
 // ---------------------------------------------------------------------------
+// Thread per B row for rows of <= 32 entries (every stencil/aggregation row):
+// the running (csi, cs) pair stays in registers and is flushed when the word
+// changes; an out-of-order word (unsorted row) merges into its earlier pair.
+// Longer rows are appended to `long_list` for the warp kernel below.
+__global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const int64_t* __restrict__ rowptr,
+                                                             const int32_t* __restrict__ cols,
+                                                             int32_t* __restrict__ csize,
+                                                             int32_t* __restrict__ csi,
+                                                             uint32_t* __restrict__ cs,
+                                                             unsigned int* long_count,
+                                                             int32_t* __restrict__ long_list)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const int64_t lo = __ldg(rowptr + j);
+        const int32_t len = static_cast<int32_t>(__ldg(rowptr + j + 1) - lo);
+        if (len > 32) {
+            long_list[atomicAdd(long_count, 1u)] = static_cast<int32_t>(j);
+            continue;
+        }
+        int32_t np = 0, cur_w = -1, maxw = -1;
+        uint32_t cur = 0;
+        for (int32_t q = 0; q < len; ++q) {
+            const int32_t c = __ldg(cols + lo + q);
+            const int32_t w = c >> 5;
+            const uint32_t bit = 1u << (c & 31);
+            if (w == cur_w) {
+                cur |= bit;
+                continue;
+            }
+            int32_t found = -1;
+            if (w <= maxw) // not beyond every word seen so far: maybe an earlier pair
+                for (int32_t t = 0; t < np; ++t)
+                    if (csi[lo + t] == w) {
+                        found = t;
+                        break;
+                    }
+            if (cur_w >= 0) { // flush the running pair
+                cs[lo + np - 1] = cur;
+                cur_w = -1;
+            }
+            if (found >= 0) { // merge into the earlier pair, in place (first-touch order kept)
+                cs[lo + found] |= bit;
+                continue;
+            }
+            csi[lo + np] = w;
+            ++np;
+            cur_w = w;
+            cur = bit;
+            maxw = max(maxw, w);
+        }
+        if (cur_w >= 0)
+            cs[lo + np - 1] = cur;
+        csize[j] = np;
+    }
+}
+
 __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ cols,
                                                        int32_t* __restrict__ csize,
                                                        int32_t* __restrict__ csi,
-                                                       uint32_t* __restrict__ cs)
+                                                       uint32_t* __restrict__ cs,
+                                                       const unsigned int* list_count,
+                                                       const int32_t* __restrict__ list)
 {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += warps) {
+    const int64_t nrows = list ? static_cast<int64_t>(*list_count) : n;
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nrows; r += warps) {
+        const int64_t j = list ? list[r] : r;
         const int64_t lo = __ldg(rowptr + j);
         const int64_t len = __ldg(rowptr + j + 1) - lo;
         if (len <= 32) {
@@ -224,16 +296,17 @@ __global__ void __launch_bounds__(256) flops_kernel(int32_t m, const int64_t* __
             f += __shfl_xor_sync(kFull, f, off, G);
             cf += __shfl_xor_sync(kFull, cf, off, G);
         }
-        if (glane == 0 && i < m) {
+        const bool owner = glane == 0 && i < m;
+        if (owner) {
             out_f[i] = f;
             out_cf[i] = cf;
             my_tf += f;
             my_tcf += cf;
             my_mf = max(my_mf, (unsigned long long)f);
             my_mcf = max(my_mcf, (unsigned long long)cf);
-            atomicAdd(&sh_hist[0][bucket_of(f)], 1ull);
-            atomicAdd(&sh_hist[1][bucket_of(cf)], 1ull);
         }
+        warp_hist_add(sh_hist[0], owner ? bucket_of(f) : -1, threadIdx.x & 31);
+        warp_hist_add(sh_hist[1], owner ? bucket_of(cf) : -1, threadIdx.x & 31);
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
@@ -504,14 +577,14 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int64_t
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const int64_t idx = base + (int64_t)k * kScanThreads + threadIdx.x;
+        int64_t v = 0;
         if (idx < n) {
-            const int64_t v = x[idx];
+            v = x[idx];
             s += v;
-            if (tot) {
-                mx = max(mx, (unsigned long long)v);
-                atomicAdd(&sh_hist[bucket_of((unsigned long long)v)], 1ull);
-            }
+            mx = max(mx, (unsigned long long)v);
         }
+        if (tot)
+            warp_hist_add(sh_hist, idx < n ? bucket_of((unsigned long long)v) : -1, threadIdx.x & 31);
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
@@ -657,10 +730,15 @@ __global__ void row_hist_kernel(int32_t m, const int64_t* __restrict__ rowptr, S
         sh_hist[t] = 0;
     __syncthreads();
     unsigned long long mx = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long v = (unsigned long long)(rowptr[i + 1] - rowptr[i]);
-        mx = max(mx, v);
-        atomicAdd(&sh_hist[bucket_of(v)], 1ull);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < m; b0 += stride) { // warp-uniform trips
+        const int64_t i = b0 + threadIdx.x;
+        unsigned long long v = 0;
+        if (i < m) {
+            v = (unsigned long long)(rowptr[i + 1] - rowptr[i]);
+            mx = max(mx, v);
+        }
+        warp_hist_add(sh_hist, i < m ? bucket_of(v) : -1, threadIdx.x & 31);
     }
     atomicMax(&tot->max_size, mx);
     __syncthreads();
@@ -777,8 +855,21 @@ cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b
 {
     if (n <= 0)
         return cudaSuccess;
-    const int blocks = (int)std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 8);
-    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs);
+    // short rows: thread per row; long rows (> 32): warp per row from a list
+    // whose length stays on the device (no host sync)
+    unsigned int* cnt = nullptr;
+    int32_t* list = nullptr;
+    cudaError_t e = cudaMallocAsync(&cnt, sizeof(unsigned int) + sizeof(int32_t) * (size_t)n, st);
+    if (e != cudaSuccess)
+        return e;
+    list = reinterpret_cast<int32_t*>(cnt + 1);
+    cudaMemsetAsync(cnt, 0, sizeof(unsigned int), st);
+    const int tblocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
+    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs, cnt, list);
+    const int blocks = sm_count() * 4;
+    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs, cnt, list);
+    count_launch();
+    cudaFreeAsync(cnt, st);
     count_launch();
     return cudaGetLastError();
 }
