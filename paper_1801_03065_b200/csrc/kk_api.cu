@@ -110,6 +110,9 @@ int host_bucket(unsigned long long x)
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kWarpSmemMax = 48 * 1024; // L1 accumulator budget per warp
+constexpr int32_t kHeavySymWords = 49152;     // 192 KB dense bitmap per CTA (heavy symbolic)
+constexpr int kHeavyLogW = 11;                // numeric heavy rows: 2048-column buckets
+constexpr int32_t kHeavyMaxBuckets = 1024;    // => k <= 2^21 for the bucketed numeric path
 constexpr uint64_t kCtaSmem = 96 * 1024;     // two CTAs per SM
 
 // device-side allocation helper (stream ordered)
@@ -485,9 +488,20 @@ struct spg_handle {
     int32_t* d_num_list = nullptr;
     DevPool num_pool;
     cudaStream_t stream = nullptr;
+    // heavy numeric rows (kk_heavy.cu): per-CTA staging for the bucket scatter
+    bool num_heavy = false;
+    int heavy_nb = 0;
+    int heavy_grid = 0;
+    int64_t heavy_cap = 0;
+    int32_t* heavy_cols = nullptr;
+    double* heavy_vals = nullptr;
 
     ~spg_handle()
     {
+        if (heavy_cols)
+            cudaFree(heavy_cols);
+        if (heavy_vals)
+            cudaFree(heavy_vals);
         if (d_rowptr)
             cudaFree(d_rowptr);
         if (d_prf)
@@ -525,6 +539,19 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
         fast = true; // forced LP: same algorithms, fast kernels
     }
     h->num = plan_phase(acc, flat, kVarNumeric, h->info.k, h->size_hist.hist, h->info.max_row_size, cfg, fast, 0);
+    // Auto: rows beyond the warp tables take the bucketed CTA path (kk_heavy.cu)
+    // when the column domain has at most kHeavyMaxBuckets buckets and a row's
+    // products fit 32-bit staging offsets
+    h->num_heavy = false;
+    if (fast && !forced && h->num.l2_class >= 0) {
+        const int64_t nb = (int64_t{h->info.k} + (1 << kHeavyLogW) - 1) >> kHeavyLogW;
+        const int64_t cap = std::max<int64_t>(h->info.flops.max_row_flops, 1);
+        if (nb <= kHeavyMaxBuckets && cap < (int64_t{1} << 31)) {
+            h->num_heavy = true;
+            h->heavy_nb = static_cast<int>(std::max<int64_t>(nb, 1));
+            h->heavy_cap = cap;
+        }
+    }
     if (h->d_num_list) {
         cudaFreeAsync(h->d_num_list, st);
         h->d_num_list = nullptr;
@@ -774,6 +801,10 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             cuda_check(cudaMemsetAsync(d_retry_cnt, 0, sizeof(unsigned long long), st), "memset");
         }
         DevPool spool;
+        // Auto: heavy rows use the CTA dense-bitmap kernel when the column
+        // domain (in 32-bit words) fits shared memory
+        const int32_t dom_words = static_cast<int32_t>((int64_t{k} + 31) / 32);
+        const int32_t heavy_words = (sfast && dom_words <= kHeavySymWords) ? std::max(dom_words, 1) : 0;
         auto sym_launch = [&](const PhaseClass& pc, const int32_t* list, int64_t nrows) {
             RowLaunch L{};
             L.a_rowptr = a->row_offsets;
@@ -792,7 +823,12 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             L.wpb = pc.wpb;
             L.grid = pc.grid;
             L.l2 = pc.l2;
-            if (pc.l2) {
+            if (pc.l2 && heavy_words > 0) {
+                // heavy rows: CTA-wide dense bitmap over the column domain
+                const int grid = static_cast<int>(std::min<int64_t>(nrows, sm_count()));
+                cuda_check(launch_symbolic_heavy(L, S.variant == kVarSymCompressed, heavy_words, grid, st),
+                           "symbolic heavy kernel");
+            } else if (pc.l2) {
                 ensure_pool(spool, S.l2, st);
                 L.pool = PoolDesc{spool.base, S.l2.chunk_bytes, S.l2.num_chunks, S.l2.pool_mode, spool.states};
                 cuda_check(launch_row_kernel(L, S.fast ? kAccLP : S.acc, S.fast ? false : S.flat, S.variant, st),
@@ -894,7 +930,7 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
         }
         cuda_check(cudaMemsetAsync(h->d_ctr, 0, sizeof(DevCounters), st), "memset");
         const PhasePlan& P = h->num;
-        if (P.l2_class >= 0)
+        if (P.l2_class >= 0 && !h->num_heavy)
             ensure_pool(h->num_pool, P.l2, st);
         for (const PhaseClass& pc : P.classes) {
             RowLaunch L{};
@@ -914,7 +950,22 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
             L.wpb = pc.wpb;
             L.grid = pc.grid;
             L.l2 = pc.l2;
-            if (pc.l2) {
+            if (pc.l2 && h->num_heavy) {
+                if (!h->heavy_cols) {
+                    // staging for the bucket scatter: one row's products per CTA,
+                    // as many CTAs as half the free memory allows (<= one per SM)
+                    size_t free_b = 0, total_b = 0;
+                    cudaMemGetInfo(&free_b, &total_b);
+                    const uint64_t per_cta = static_cast<uint64_t>(h->heavy_cap) * 12;
+                    const int64_t fit = static_cast<int64_t>((free_b / 2) / std::max<uint64_t>(per_cta, 1));
+                    h->heavy_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({fit, sm_count(), pc.count})));
+                    h->heavy_cols = dalloc<int32_t>(static_cast<size_t>(h->heavy_cap) * h->heavy_grid, st, "heavy staging");
+                    h->heavy_vals = dalloc<double>(static_cast<size_t>(h->heavy_cap) * h->heavy_grid, st, "heavy staging");
+                }
+                cuda_check(launch_numeric_heavy(L, h->heavy_cols, h->heavy_vals, h->heavy_cap, kHeavyLogW, h->heavy_nb,
+                                                h->heavy_grid, st),
+                           "numeric heavy kernel");
+            } else if (pc.l2) {
                 L.pool = PoolDesc{h->num_pool.base, P.l2.chunk_bytes, P.l2.num_chunks, P.l2.pool_mode,
                                   h->num_pool.states};
                 cuda_check(launch_row_kernel(L, P.fast ? kAccLP : P.acc, P.fast ? false : P.flat, kVarNumeric, st),

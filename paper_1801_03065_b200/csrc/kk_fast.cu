@@ -234,6 +234,57 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
 }
 
 // ---------------------------------------------------------------------------
+// Thread-Flat-Parallel index mapping.  For one chunk of <= 32 A entries the
+// flattened product index t maps to (segment, offset) = flat_position(prefix, t)
+// (engine.cpp:360-365).  Instead of a 5-step shuffle binary search per window,
+// the non-empty segments are compacted once per chunk (their starts are then
+// strictly increasing) and, per 32-product window, the segment starts falling
+// inside the window form a bit mask M: lane x's segment is (segments started
+// before the window) + popc(M & lanes<=x) - 1.
+// ---------------------------------------------------------------------------
+struct FlatMap {
+    int64_t cbase;  // compacted: lane c holds the B-row base of the c-th non-empty segment
+    double ca;      // ... its A value
+    int32_t cexcl;  // ... its start in the flattened index space
+    int32_t nne;    // non-empty segments
+    int32_t rank;   // non-empty segments starting before the current window
+    int32_t total;  // products of the chunk
+
+    __device__ __forceinline__ void init(int64_t bb, int32_t bl, double av, int lane)
+    {
+        int32_t incl = bl;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, incl, off);
+            if (lane >= off)
+                incl += y;
+        }
+        const int32_t excl = incl - bl;
+        total = __shfl_sync(kFull, incl, 31);
+        const uint32_t ne = __ballot_sync(kFull, bl > 0);
+        nne = __popc(ne);
+        const int src = lane < nne ? static_cast<int>(__fns(ne, 0, lane + 1)) : lane;
+        cbase = __shfl_sync(kFull, bb, src);
+        ca = __shfl_sync(kFull, av, src);
+        cexcl = __shfl_sync(kFull, excl, src);
+        rank = 0;
+    }
+
+    // segment data of this lane's product in window [w0, w0+32); advances rank
+    __device__ __forceinline__ void window(int32_t w0, int lane, int32_t& e, int64_t& base, double& a)
+    {
+        const uint32_t bit = (lane < nne && cexcl >= w0 && cexcl < w0 + 32) ? (1u << (cexcl - w0)) : 0u;
+        const uint32_t M = __reduce_or_sync(kFull, bit);
+        int seg = rank + __popc(M & ((2u << lane) - 1u)) - 1;
+        seg = seg < 0 ? 0 : (seg > 31 ? 31 : seg);
+        e = __shfl_sync(kFull, cexcl, seg);
+        base = __shfl_sync(kFull, cbase, seg);
+        a = __shfl_sync(kFull, ca, seg);
+        rank += __popc(M);
+    }
+};
+
+// ---------------------------------------------------------------------------
 // numeric: LP + Thread-Flat-Parallel (short B rows)
 // ---------------------------------------------------------------------------
 // One 32-product window of the row's flattened multiplications (engine.cpp:
@@ -328,27 +379,15 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
             }
             // flattened prefix of this chunk's B-row lengths (32-bit: one
             // chunk of a flat-scheme row never holds 2^31 products)
-            int32_t incl = bl;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int32_t y = __shfl_up_sync(kFull, incl, off);
-                if (lane >= off)
-                    incl += y;
-            }
-            const int32_t excl = incl - bl;
-            const int32_t total = __shfl_sync(kFull, incl, 31);
+            FlatMap fm;
+            fm.init(bb, bl, av, lane);
+            const int32_t total = fm.total;
             for (int32_t w0 = 0; w0 < total; w0 += 32) {
                 const int32_t t = w0 + lane;
-                int seg = 0; // upper_bound(prefix, t) - 1 (flat_position, engine.cpp:360-365)
-#pragma unroll
-                for (int s = 16; s >= 1; s >>= 1) {
-                    const int32_t y = __shfl_sync(kFull, incl, seg + s - 1);
-                    if (y <= t)
-                        seg += s;
-                }
-                const int32_t e = __shfl_sync(kFull, excl, seg);
-                const int64_t base = __shfl_sync(kFull, bb, seg);
-                const double a = __shfl_sync(kFull, av, seg);
+                int32_t e;
+                int64_t base;
+                double a;
+                fm.window(w0, lane, e, base, a);
                 const bool valid = t < total;
                 int32_t key = 0;
                 double v = 0.0;
@@ -442,31 +481,20 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                 bb = __ldg(b_rowptr + j);
                 bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
             }
-            int32_t incl = bl;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int32_t y = __shfl_up_sync(kFull, incl, off);
-                if (lane >= off)
-                    incl += y;
-            }
-            const int32_t excl = incl - bl;
-            const int32_t total = __shfl_sync(kFull, incl, 31);
-            for (int32_t w0 = 0; w0 < total; w0 += 32) {
+            FlatMap fm;
+            fm.init(bb, bl, 0.0, lane);
+            const int32_t total = fm.total;
+            // window w0's (key, word) are loaded one window ahead
+            auto fetch = [&](int32_t w0, int32_t& key, uint32_t& word) {
                 const int32_t t = w0 + lane;
-                int seg = 0;
-#pragma unroll
-                for (int s = 16; s >= 1; s >>= 1) {
-                    const int32_t y = __shfl_sync(kFull, incl, seg + s - 1);
-                    if (y <= t)
-                        seg += s;
-                }
-                const int32_t e = __shfl_sync(kFull, excl, seg);
-                const int64_t base = __shfl_sync(kFull, bb, seg);
-                bool claimed = false;
+                int32_t e;
+                int64_t base;
+                double a_unused;
+                fm.window(w0, lane, e, base, a_unused);
+                key = kEmpty;
+                word = 0u;
                 if (t < total) {
                     const int64_t q = base + (t - e);
-                    int32_t key;
-                    uint32_t word;
                     if constexpr (kCompressed) {
                         key = __ldg(L.csi + q);
                         word = __ldg(L.cs + q);
@@ -474,6 +502,18 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                         key = __ldg(L.b_cols + q);
                         word = 1u;
                     }
+                }
+            };
+            int32_t nkey;
+            uint32_t nword;
+            fetch(0, nkey, nword);
+            for (int32_t w0 = 0; w0 < total; w0 += 32) {
+                const int32_t key = nkey;
+                const uint32_t word = nword;
+                if (w0 + 32 < total)
+                    fetch(w0 + 32, nkey, nword);
+                bool claimed = false;
+                if (key != kEmpty) {
                     uint32_t s = loc_hash(key, pshift);
                     for (int probes = 0; probes <= T; ++probes) {
                         const int32_t k = keys[s];

@@ -108,6 +108,11 @@ cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, unsigned l
                                  int32_t* retry_list, cudaStream_t st);
 int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem);
 
+// heavy rows (kk_heavy.cu)
+cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st);
+cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double* stage_vals, int64_t stage_cap,
+                                 int32_t logw, int32_t nb, int grid, cudaStream_t st);
+
 void count_launch(int n = 1);
 int sm_count();
 

@@ -81,7 +81,11 @@ __device__ __forceinline__ uint32_t group_or(uint32_t grp, uint32_t v, int lane)
 // for sorted rows; unsorted long rows use an order-insensitive merge (the
 // compressed graph only feeds the order-independent bit-OR union).
 // ---------------------------------------------------------------------------
-// Thread per B row for rows of <= 32 entries (every stencil/aggregation row):
+// rows up to this length are compressed by one thread (aggregation/AP rows);
+// longer ones (stencils: 27) by a warp, whose loads coalesce
+constexpr int32_t kShortRow = 8;
+
+// Thread per B row for rows of <= kShortRow entries:
 // the running (csi, cs) pair stays in registers and is flushed when the word
 // changes; an out-of-order word (unsorted row) merges into its earlier pair.
 // Longer rows are appended to `long_list` for the warp kernel below.
@@ -94,13 +98,28 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const in
                                                              int32_t* __restrict__ long_list)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        const int64_t lo = __ldg(rowptr + j);
-        const int32_t len = static_cast<int32_t>(__ldg(rowptr + j + 1) - lo);
-        if (len > 32) {
-            long_list[atomicAdd(long_count, 1u)] = static_cast<int32_t>(j);
-            continue;
+    const int lane = threadIdx.x & 31;
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += stride) { // warp-uniform trips
+        const int64_t j = b0 + threadIdx.x;
+        int64_t lo = 0;
+        int32_t len = 0;
+        if (j < n) {
+            lo = __ldg(rowptr + j);
+            len = static_cast<int32_t>(__ldg(rowptr + j + 1) - lo);
         }
+        // rows beyond kShortRow go to the warp kernel (warp-aggregated append)
+        const bool is_long = j < n && len > kShortRow;
+        const uint32_t lm = __ballot_sync(kFull, is_long);
+        if (lm) {
+            unsigned int base = 0;
+            if (lane == __ffs(lm) - 1)
+                base = atomicAdd(long_count, static_cast<unsigned int>(__popc(lm)));
+            base = __shfl_sync(kFull, base, __ffs(lm) - 1);
+            if (is_long)
+                long_list[base + __popc(lm & lanemask_lt())] = static_cast<int32_t>(j);
+        }
+        if (j >= n || is_long)
+            continue;
         int32_t np = 0, cur_w = -1, maxw = -1;
         uint32_t cur = 0;
         for (int32_t q = 0; q < len; ++q) {
