@@ -111,8 +111,8 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kWarpSmemMax = 48 * 1024; // L1 accumulator budget per warp
 constexpr int32_t kHeavySymWords = 49152;     // 192 KB dense bitmap per CTA (heavy symbolic)
-constexpr int kHeavyLogW = 11;                // numeric heavy rows: 2048-column buckets
-constexpr int32_t kHeavyMaxBuckets = 1024;    // => k <= 2^21 for the bucketed numeric path
+constexpr int kHeavyLogW = 10;                // numeric heavy rows: 1024-column buckets
+constexpr int32_t kHeavyMaxBuckets = 1024;    // => k <= 2^20 for the bucketed numeric path
 constexpr uint64_t kCtaSmem = 96 * 1024;     // two CTAs per SM
 
 // device-side allocation helper (stream ordered)
@@ -958,7 +958,8 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
                     cudaMemGetInfo(&free_b, &total_b);
                     const uint64_t per_cta = static_cast<uint64_t>(h->heavy_cap) * 12;
                     const int64_t fit = static_cast<int64_t>((free_b / 2) / std::max<uint64_t>(per_cta, 1));
-                    h->heavy_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({fit, sm_count(), pc.count})));
+                    // two CTAs per SM fit (hist and slabs share shared memory)
+                    h->heavy_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({fit, 2 * sm_count(), pc.count})));
                     h->heavy_cols = dalloc<int32_t>(static_cast<size_t>(h->heavy_cap) * h->heavy_grid, st, "heavy staging");
                     h->heavy_vals = dalloc<double>(static_cast<size_t>(h->heavy_cap) * h->heavy_grid, st, "heavy staging");
                 }

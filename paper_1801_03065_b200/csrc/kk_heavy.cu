@@ -174,38 +174,104 @@ struct HeavyArgs {
     int32_t nb;          // buckets (k / W rounded up)
 };
 
+// block-wide exclusive scan of one int32 per thread (kHeavyThreads threads);
+// returns the exclusive prefix, *total gets the sum
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sh_warp, int32_t* total)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o)
+            incl += y;
+    }
+    if (lane == 31)
+        sh_warp[warp] = incl;
+    __syncthreads();
+    int32_t wpre = 0, tot = 0;
+    for (int w = 0; w < kHeavyWarps; ++w) {
+        const int32_t x = sh_warp[w];
+        wpre += w < warp ? x : 0;
+        tot += x;
+    }
+    *total = tot;
+    __syncthreads();
+    return wpre + incl - v;
+}
+
 __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowLaunch L, const HeavyArgs H)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nb = H.nb;
     const int W = 1 << H.logw;
-    // layout: off[kHeavyWarps][nb] int32 | bstart[nb+1] int32 | bcount[nb] int32 |
-    //         per-warp dense slab vals[W] double + bitmap[W/32]
-    int32_t* off = reinterpret_cast<int32_t*>(smem);
-    int32_t* bstart = off + kHeavyWarps * nb;
+    // layout: bstart[nb+1] | bcount[nb] | outoff[nb] (int32) | union {
+    //   off[kHeavyWarps][nb] int32            (passes 1-2: tile x bucket offsets)
+    //   per-warp dense slab vals[W] + bitmap  (pass 3) }
+    // The union keeps the CTA small enough for two CTAs per SM.
+    int32_t* bstart = reinterpret_cast<int32_t*>(smem);
     int32_t* bcount = bstart + nb + 1;
-    const size_t head = ((size_t)(kHeavyWarps * nb + 2 * nb + 1) * 4 + 15) / 16 * 16;
+    int32_t* outoff = bcount + nb;
+    const size_t head = ((size_t)(3 * nb + 1) * 4 + 15) / 16 * 16;
+    int32_t* off = reinterpret_cast<int32_t*>(smem + head);
     double* slab = reinterpret_cast<double*>(smem + head) + (size_t)warp * W;
     uint32_t* bits = reinterpret_cast<uint32_t*>(smem + head + (size_t)kHeavyWarps * W * 8) + (size_t)warp * (W / 32);
+    __shared__ int32_t sh_warp[kHeavyWarps];
+    __shared__ int64_t tile_lo[kHeavyWarps + 1];
+    __shared__ int32_t next_bucket;
     __shared__ int32_t s_total;
     int32_t* scols = H.stage_cols + (size_t)blockIdx.x * H.stage_cap;
     double* svals = H.stage_vals + (size_t)blockIdx.x * H.stage_cap;
-    for (int t = lane; t < W / 32; t += 32)
-        bits[t] = 0u;
 
     for (int64_t r = blockIdx.x; r < L.nrows; r += gridDim.x) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
         const int64_t cbase = __ldg(L.c_rowptr + i);
         const int32_t cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
         const int64_t abeg = __ldg(L.a_rowptr + i), aend = __ldg(L.a_rowptr + i + 1);
-        // contiguous A-entry tile per warp: tiles in warp order = product order
         const int64_t d = aend - abeg;
-        const int64_t t_lo = abeg + d * warp / kHeavyWarps, t_hi = abeg + d * (warp + 1) / kHeavyWarps;
+        // ---- product-balanced contiguous tiles of A entries, one per warp ----
+        // thread t owns A entries [abeg + d*t/T, abeg + d*(t+1)/T)
+        const int64_t e_lo = abeg + d * threadIdx.x / kHeavyThreads;
+        const int64_t e_hi = abeg + d * (threadIdx.x + 1) / kHeavyThreads;
+        int32_t mine = 0;
+        for (int64_t p = e_lo; p < e_hi; ++p) {
+            const int32_t j = __ldg(L.a_cols + p);
+            mine += static_cast<int32_t>(__ldg(L.b_rowptr + j + 1) - __ldg(L.b_rowptr + j));
+        }
+        if (threadIdx.x <= kHeavyWarps)
+            tile_lo[threadIdx.x] = threadIdx.x == 0 ? abeg : aend;
+        int32_t F;
+        const int32_t before = block_excl_scan(mine, sh_warp, &F);
+        if (threadIdx.x == 0) {
+            s_total = F;
+            next_bucket = 0;
+        }
+        // tile w starts at the first A entry p whose product prefix P(p) >= F*w/8
+        for (int w = 1; w < kHeavyWarps; ++w) {
+            const int64_t target = static_cast<int64_t>(F) * w / kHeavyWarps;
+            long long cand = aend;
+            if (before >= target) {
+                cand = e_lo;
+            } else if (before + mine >= target) {
+                int64_t run = before;
+                for (int64_t p = e_lo; p < e_hi; ++p) {
+                    if (run >= target) {
+                        cand = p;
+                        break;
+                    }
+                    const int32_t j = __ldg(L.a_cols + p);
+                    run += __ldg(L.b_rowptr + j + 1) - __ldg(L.b_rowptr + j);
+                }
+            }
+            if (cand < aend)
+                atomicMin(reinterpret_cast<long long*>(&tile_lo[w]), cand);
+        }
         for (int t = threadIdx.x; t < kHeavyWarps * nb; t += blockDim.x)
             off[t] = 0;
         __syncthreads();
-        // pass 1: per-(tile, bucket) counts
+        const int64_t t_lo = tile_lo[warp], t_hi = tile_lo[warp + 1];
+        // ---- pass 1: per-(tile, bucket) counts ----
         walk_products<true, false>(L, t_lo, t_hi, lane, [&](bool valid, int32_t key, uint32_t, double) {
             const int b = valid ? (key >> H.logw) : -1;
             const uint32_t grp = __match_any_sync(kFull, b);
@@ -213,40 +279,41 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
                 off[warp * nb + b] += __popc(grp);
         });
         __syncthreads();
-        // bucket-major exclusive scan -> stable offsets off[w][b]
-        if (warp == 0) {
-            int32_t carry = 0;
-            for (int b0 = 0; b0 < nb; b0 += 32) {
-                const int b = b0 + lane;
-                int32_t tot = 0;
+        // ---- bucket-major exclusive scan -> stable offsets off[w][b] ----
+        {
+            constexpr int kPer = 4; // buckets per thread (nb <= 1024)
+            int32_t tot[kPer];
+            int32_t mysum = 0;
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int b = threadIdx.x * kPer + u;
+                tot[u] = 0;
                 if (b < nb)
                     for (int w = 0; w < kHeavyWarps; ++w)
-                        tot += off[w * nb + b];
-                int32_t incl = tot;
+                        tot[u] += off[w * nb + b];
+                mysum += tot[u];
+            }
+            int32_t all;
+            int32_t run = block_excl_scan(mysum, sh_warp, &all);
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int32_t y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o)
-                        incl += y;
-                }
+            for (int u = 0; u < kPer; ++u) {
+                const int b = threadIdx.x * kPer + u;
                 if (b < nb) {
-                    int32_t run = carry + incl - tot;
                     bstart[b] = run;
+                    int32_t rr = run;
                     for (int w = 0; w < kHeavyWarps; ++w) {
                         const int32_t c = off[w * nb + b];
-                        off[w * nb + b] = run;
-                        run += c;
+                        off[w * nb + b] = rr;
+                        rr += c;
                     }
                 }
-                carry += __shfl_sync(kFull, incl, 31);
+                run += tot[u];
             }
-            if (lane == 0) {
-                bstart[nb] = carry;
-                s_total = carry;
-            }
+            if (threadIdx.x == 0)
+                bstart[nb] = all;
         }
         __syncthreads();
-        // pass 2: stable scatter of (col, a*b) into the CTA's staging area
+        // ---- pass 2: stable scatter of (col, a*b) into the CTA's staging ----
         walk_products<true, false>(L, t_lo, t_hi, lane, [&](bool valid, int32_t key, uint32_t, double v) {
             const int b = valid ? (key >> H.logw) : -1;
             const uint32_t grp = __match_any_sync(kFull, b);
@@ -264,17 +331,40 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             }
         });
         __syncthreads();
-        // pass 3: each warp accumulates whole buckets, in product order
-        for (int b = warp; b < nb; b += kHeavyWarps) {
+        // ---- pass 3: warps grab buckets dynamically; ordered dense accumulation ----
+        for (int t = lane; t < W / 32; t += 32) // the slab region aliased off[] in passes 1-2
+            bits[t] = 0u;
+        __syncwarp();
+        for (;;) {
+            int b = 0;
+            if (lane == 0)
+                b = atomicAdd(&next_bucket, 1);
+            b = __shfl_sync(kFull, b, 0);
+            if (b >= nb)
+                break;
             const int32_t lo = bstart[b], hi = bstart[b + 1];
+            if (lo == hi) {
+                if (lane == 0)
+                    bcount[b] = 0;
+                continue;
+            }
+            int32_t nkey = -1 - lane;
+            double nv = 0.0;
+            if (lo + lane < hi) {
+                nkey = scols[lo + lane] & (W - 1);
+                nv = svals[lo + lane];
+            }
             for (int32_t w0 = lo; w0 < hi; w0 += 32) {
                 const int32_t q = w0 + lane;
                 const bool valid = q < hi;
-                int32_t key = -1 - lane;
-                double v = 0.0;
-                if (valid) {
-                    key = scols[q] & (W - 1);
-                    v = svals[q];
+                const int32_t key = nkey;
+                const double v = nv;
+                // next window's products are loaded while this one accumulates
+                nkey = -1 - lane;
+                nv = 0.0;
+                if (q + 32 < hi) {
+                    nkey = scols[q + 32] & (W - 1);
+                    nv = svals[q + 32];
                 }
                 const uint32_t grp = __match_any_sync(kFull, key);
                 const bool leader = valid && (__ffs(grp) - 1) == lane;
@@ -331,29 +421,31 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             __syncwarp();
         }
         __syncthreads();
-        // output offsets of the buckets; then copy out
-        if (warp == 0) {
-            int32_t carry = 0;
-            for (int b0 = 0; b0 < nb; b0 += 32) {
-                const int b = b0 + lane;
-                const int32_t c = b < nb ? bcount[b] : 0;
-                int32_t incl = c;
+        // ---- output offsets of the buckets, then copy out ----
+        {
+            constexpr int kPer = 4;
+            int32_t mysum = 0;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int32_t y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o)
-                        incl += y;
-                }
-                if (b < nb)
-                    off[b] = carry + incl - c; // reuse: output offset of bucket b
-                carry += __shfl_sync(kFull, incl, 31);
+            for (int u = 0; u < kPer; ++u) {
+                const int b = threadIdx.x * kPer + u;
+                mysum += b < nb ? bcount[b] : 0;
             }
-            if (lane == 0 && carry != cap)
-                raise_error(L.ctr, carry < cap ? kDevRowShort : kDevRowOverflow);
+            int32_t all;
+            int32_t run = block_excl_scan(mysum, sh_warp, &all);
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int b = threadIdx.x * kPer + u;
+                if (b < nb) {
+                    outoff[b] = run;
+                    run += bcount[b];
+                }
+            }
+            if (threadIdx.x == 0 && all != cap)
+                raise_error(L.ctr, all < cap ? kDevRowShort : kDevRowOverflow);
         }
         __syncthreads();
         for (int b = warp; b < nb; b += kHeavyWarps) {
-            const int32_t lo = bstart[b], c = bcount[b], o = off[b];
+            const int32_t lo = bstart[b], c = bcount[b], o = outoff[b];
             for (int32_t q = lane; q < c; q += 32) {
                 if (o + q < cap) {
                     L.c_cols[cbase + o + q] = scols[lo + q];
@@ -372,8 +464,10 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
 // ---------------------------------------------------------------------------
 size_t heavy_numeric_smem(int nb, int logw)
 {
-    const size_t head = ((size_t)(kHeavyWarps * nb + 2 * nb + 1) * 4 + 15) / 16 * 16;
-    return head + (size_t)kHeavyWarps * ((size_t(1) << logw) * 8 + (size_t(1) << logw) / 8);
+    const size_t head = ((size_t)(3 * nb + 1) * 4 + 15) / 16 * 16;
+    const size_t hist = (size_t)kHeavyWarps * nb * 4;
+    const size_t slabs = (size_t)kHeavyWarps * ((size_t(1) << logw) * 8 + (size_t(1) << logw) / 8);
+    return head + (hist > slabs ? hist : slabs);
 }
 
 cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st)
