@@ -4,13 +4,17 @@
 //
 // numeric_lp_seq_kernel   Thread-Sequential numeric Gustavson (engine.cpp:259-267)
 //     with a linear-probing L1 table in shared memory (keys[T], vals[T] by
-//     slot, slot_of[] by first-touch position) under a locality-preserving
-//     hash, so the entries of one B row (runs of consecutive columns on
-//     stencils) land in distinct banks.  New keys claim slots with a
-//     write-then-verify round instead of shared-memory CAS.  B rows of the
-//     next steps are prefetched into registers one batch ahead.  Positions
-//     are assigned in lane (= first-touch) order and values summed left to
-//     right with unfused mul/add, so C is bitwise the reference's output.
+//     slot, slot_of[] by first-touch position, Fibonacci hash).  New keys
+//     claim slots with one shared CAS (a write-then-verify variant exists,
+//     KK_NUM_VERIFY, measured slower).  Per-step scalars of the A chunk are
+//     staged in shared memory and B rows of step q+2 are prefetched into
+//     registers while step q accumulates.  Positions are assigned in lane
+//     (= first-touch) order and values summed left to right with unfused
+//     mul/add, so C is bitwise the reference's output.
+//
+// numeric_lp_flat_kernel  Thread-Flat-Parallel numeric for short B rows: 32-product
+//     windows, duplicate keys grouped with __match_any_sync and folded by the
+//     lowest lane in lane (= product) order onto the running sum.
 //
 // symbolic_flat_kernel    Thread-Flat-Parallel structure union (engine.cpp:268-286
 //     with SymbolicSink :210-221) over the compressed graph (or raw columns).

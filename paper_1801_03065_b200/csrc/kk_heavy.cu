@@ -88,28 +88,43 @@ __device__ __forceinline__ void walk_products(const RowLaunch& L, int64_t p_lo, 
         }
         HMap fm;
         fm.init(bb, bl, av, lane);
-        for (int32_t w0 = 0; w0 < fm.total; w0 += 32) {
+        // window loads are issued one window ahead of their use (latency hiding:
+        // these kernels run at two CTAs of 8 warps per SM)
+        auto load = [&](int32_t w0, int32_t& key, uint32_t& word, double& v) {
             int32_t e;
             int64_t base;
             double a;
             fm.window(w0, lane, e, base, a);
             const int32_t t = w0 + lane;
-            const bool valid = t < fm.total;
-            int32_t key = 0;
-            uint32_t word = 0;
-            double v = 0.0;
-            if (valid) {
+            key = 0;
+            word = 0;
+            v = 0.0;
+            if (t < fm.total) {
                 const int64_t q = base + (t - e);
                 if constexpr (kCompressed) {
                     key = __ldg(L.csi + q);
                     word = __ldg(L.cs + q);
                 } else {
-                    key = __ldg(L.b_cols + q);
-                    word = 1u << (key & 31);
+                    key = __ldg(L.b_cols + q); // raw column: its word bit is set at use
                     if constexpr (kNumeric)
                         v = __dmul_rn(a, __ldg(L.b_vals + q));
                 }
             }
+        };
+        int32_t nkey;
+        uint32_t nword;
+        double nv;
+        if (fm.total > 0)
+            load(0, nkey, nword, nv);
+        for (int32_t w0 = 0; w0 < fm.total; w0 += 32) {
+            const int32_t key = nkey;
+            uint32_t word = nword;
+            const double v = nv;
+            const bool valid = w0 + lane < fm.total;
+            if (w0 + 32 < fm.total)
+                load(w0 + 32, nkey, nword, nv);
+            if constexpr (!kCompressed)
+                word = 1u << (key & 31);
             fn(valid, key, word, v);
         }
     }
