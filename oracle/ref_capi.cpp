@@ -18,6 +18,7 @@
 #include <random>
 #include <string>
 
+#include "spgemm/bench.hpp"
 #include "spgemm/compression.hpp"
 #include "spgemm/csr_matrix.hpp"
 #include "spgemm/engine.hpp"
@@ -358,6 +359,13 @@ double ref_multiply_ms(void* a, void* b, const ref_cfg* cfg, int64_t* nnz_c)
             *nnz_c = r.c.nnz();
     });
     return ms;
+}
+
+// the reference's results reader + Dolan-Moré profile (bench.cpp:55-175), as
+// cli.cpp:291-298 chains them; returns 0 or the guard code
+int ref_profile_csv(const char* in, const char* out, int points)
+{
+    return guard([&] { write_profile_csv(out, compute_profile(read_bench_csv(in), points)); });
 }
 
 // gustavson_serial multiplication count (oracle.cpp:9-48)
