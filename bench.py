@@ -204,9 +204,18 @@ def main():
     import torch.distributed as dist
     import paper_1801_03065_b200 as kk
 
+    # one process per GPU over NCCL; KK_BENCH_BACKEND=gloo (with KK_BENCH_SAME_GPU=1)
+    # runs the multi-rank code path on a single GPU as a smoke test (host
+    # collectives only: no rank's kernel waits on another's)
+    backend = os.environ.get("KK_BENCH_BACKEND", "nccl")
+    if os.environ.get("KK_BENCH_SAME_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
@@ -360,7 +369,7 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl, "mode": "symbolic+numeric (NoReuse multiply per step)",
                    "m": m, "nnz_a": nnz_a, "flops": int(flops), "nnz_c": int(nnz_c),
-                   "parallelism": f"row-shard x{world}" + (" + NCCL broadcast of B" if args.broadcast else
+                   "parallelism": f"row-shard x{world}" + (f" + {backend} broadcast of B" if args.broadcast else
                                                             " (B resident)"),
                    "l2_policy": "inputs larger than L2 (A = %.2f GB > 126 MB)" % (nnz_a * 12 / 1e9)},
         "numeric_only": {"value": value_num, "unit": UNIT, "ms_per_step": ms_num},
