@@ -91,19 +91,21 @@ __device__ __forceinline__ void num_step(bool valid, int32_t key, double v, int3
     }
     const uint32_t nm = __ballot_sync(kFull, is_new);
     if (nm) {
+        // keys beyond the symbolic row size are never inserted (the row is in
+        // error, reported at its end): the table keeps free slots, probes end
+        const int32_t pos = cnt + __popc(nm & lanemask_lt());
+        const bool claim = is_new && pos < cap;
         if constexpr (kCas) {
-            if (is_new)
+            if (claim)
                 while (atomicCAS(&keys[s], kEmpty, key) != kEmpty)
                     s = (s + kProbeStep) & tmask;
         } else {
             __syncwarp();
-            s = claim_slots(is_new, key, s, keys, tmask);
+            s = claim_slots(claim, key, s, keys, tmask);
         }
-        if (is_new) {
-            const int32_t pos = cnt + __popc(nm & lanemask_lt());
+        if (claim) {
             vals[s] = v;
-            if (pos < cap)
-                slot_of[pos] = static_cast<int32_t>(s);
+            slot_of[pos] = static_cast<int32_t>(s);
         }
         cnt += __popc(nm);
     }
@@ -318,13 +320,14 @@ __device__ __forceinline__ void num_window(bool valid, int32_t key, double v, in
             is_new = true;
     }
     const uint32_t nm = __ballot_sync(kFull, is_new);
+    bool claimed = false;
     if (nm) {
-        if (is_new) {
+        const int32_t pos = cnt + __popc(nm & lanemask_lt());
+        if (is_new && pos < cap) { // beyond the symbolic row size: never inserted
             while (atomicCAS(&keys[s], kEmpty, key) != kEmpty)
                 s = (s + kProbeStep) & tmask;
-            const int32_t pos = cnt + __popc(nm & lanemask_lt());
-            if (pos < cap)
-                slot_of[pos] = static_cast<int32_t>(s);
+            slot_of[pos] = static_cast<int32_t>(s);
+            claimed = true;
         }
         cnt += __popc(nm);
     }
@@ -338,7 +341,7 @@ __device__ __forceinline__ void num_window(bool valid, int32_t key, double v, in
             rest &= rest - 1;
         }
     }
-    if (leader)
+    if (leader && (!is_new || claimed))
         vals[s] = acc;
     __syncwarp();
 }

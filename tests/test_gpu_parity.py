@@ -201,6 +201,24 @@ def test_reuse_rejects_mismatch(kk):
         kk.numeric(trimmed, b, h)
 
 
+def test_structure_mismatch_is_reported_not_hung(kk):
+    """Same dimensions and nnz but a different B structure: the reference throws
+    logic_error (engine.cpp:238-245); the kernels must report it, never spin."""
+    rng = np.random.default_rng(11)
+    for flat in (False, True):
+        n = 40 if not flat else 400
+        a = random_csr(rng, 30, n, 0.3 if not flat else 0.02)
+        b = random_csr(rng, n, 50, 0.2)
+        h = kk.symbolic(a, b)
+        # move every entry of B to column 0..: same nnz, far fewer distinct columns
+        b2 = kk.CsrMatrix(b.num_rows, b.num_cols, b.row_offsets, b.col_indices.copy(), b.values, False)
+        for i in range(b2.num_rows):
+            lo, hi = b2.row_offsets[i], b2.row_offsets[i + 1]
+            b2.col_indices[lo:hi] = (np.arange(hi - lo) * 7 + i) % b2.num_cols
+        with pytest.raises(kk.InternalError):
+            kk.numeric(a, b2, h, kk.PhaseStats())
+
+
 def test_contract_errors(kk):
     a = csr_from_triplets(2, 3, [])
     b = csr_from_triplets(2, 2, [])
