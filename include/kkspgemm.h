@@ -211,6 +211,12 @@ int spg_sort_rows(int32_t m, const int64_t* d_row_offsets, int32_t* d_cols, doub
  * flop-balanced row partition of the multi-GPU path. */
 int spg_row_flops(const spg_csr* a, const spg_csr* b, int64_t* d_out, void* stream);
 
+/* Structure-reuse replay state of a handle (extension, no reference
+ * counterpart): 0 = the handle runs the hashing kernels only, 1 = eligible
+ * (the slot map is recorded on the second numeric pass), 2 = recorded (later
+ * passes replay it while A's and B's structure fingerprints match). */
+int spg_handle_replay_state(spg_handle_t h);
+
 /* Number of kernels this library launched since load (evidence counter). */
 int64_t spg_kernel_launch_count(void);
 

@@ -158,7 +158,7 @@ EXPORTED_SYMBOLS = (
     "spg_symbolic", "spg_numeric", "spg_handle_info_get", "spg_handle_copy_row_offsets",
     "spg_handle_copy_per_row_flops", "spg_handle_copy_row_offsets_device", "spg_handle_set_numeric", "spg_handle_import",
     "spg_handle_check", "spg_handle_destroy", "spg_sort_rows", "spg_kernel_launch_count",
-    "spg_row_flops",
+    "spg_row_flops", "spg_handle_replay_state",
 )
 
 _lib_handle = None
@@ -175,6 +175,8 @@ def lib() -> C.CDLL:
         L.spg_last_error.restype = C.c_char_p
         L.spg_kernel_launch_count.restype = C.c_int64
         L.spg_handle_destroy.restype = None
+        L.spg_handle_replay_state.restype = C.c_int
+        L.spg_handle_replay_state.argtypes = [C.c_void_p]
         for name in ("spg_config_init", "spg_resolve_config", "spg_flat_position", "spg_symbolic",
                      "spg_numeric", "spg_handle_info_get", "spg_handle_copy_row_offsets",
                      "spg_handle_copy_per_row_flops", "spg_handle_copy_row_offsets_device", "spg_handle_set_numeric",
@@ -395,6 +397,11 @@ class SpgemmHandle:
 
     @property
     def max_row_size(self): return int(self._info().max_row_size)
+
+    @property
+    def replay_state(self) -> int:
+        """0 hashing only, 1 replay eligible, 2 slot map recorded (kk_replay.cu)."""
+        return int(lib().spg_handle_replay_state(self._ptr))
     @property
     def avg_row_size(self): return float(self._info().avg_row_size)
     @property

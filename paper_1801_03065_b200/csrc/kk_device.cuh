@@ -32,6 +32,7 @@ enum DevError : int {
     kDevRowShort = 2,     // numeric row shorter than the structure (engine.cpp:244-245)
     kDevKeyRange = 3,     // key outside the dense domain (accumulators.hpp:308-309)
     kDevL2Overflow = 4,   // level-2 bound violated (engine.cpp:83-84)
+    kDevReplay = 5,       // slot-replay map does not match the structure (kk_replay.cu)
 };
 
 struct DevCounters {

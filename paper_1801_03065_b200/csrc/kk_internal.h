@@ -113,6 +113,32 @@ cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t w
 cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double* stage_vals, int64_t stage_cap,
                                  int32_t logw, int32_t nb, int grid, cudaStream_t st);
 
+// structure-reuse replay (kk_replay.cu)
+struct ReplayLaunch {
+    const int64_t* a_rowptr;
+    const int32_t* a_cols;
+    const double* a_vals;
+    const int64_t* b_rowptr;
+    const int32_t* b_cols;
+    const double* b_vals;
+    const int64_t* c_rowptr;
+    int32_t* c_cols;
+    double* c_vals;
+    int32_t* ccache;          // C columns in first-touch order
+    void* map;                // uint8_t / uint16_t slot per product
+    const int64_t* prod_off;  // [m+1] first product of each row
+    int64_t m;
+    DevCounters* ctr;
+    int32_t T;                // build: per-warp hash size (pow2 >= 2 * max row)
+    int shift;                // build: 32 - log2(T)
+    int wpb;
+    uint64_t warp_bytes;
+};
+cudaError_t launch_fingerprint(int64_t rows, const int64_t* rowptr, const int32_t* cols, uint64_t salt,
+                               unsigned long long* out, cudaStream_t st);
+cudaError_t launch_replay_build(ReplayLaunch R, int width, cudaStream_t st);
+cudaError_t launch_replay_numeric(ReplayLaunch R, int width, int32_t max_row, cudaStream_t st);
+
 void count_launch(int n = 1);
 int sm_count();
 

@@ -1,0 +1,336 @@
+// Structure-reuse replay of the numeric phase (sm_100a).
+//
+// The reference's reuse contract (engine.hpp:42-56, cli.cpp:137-151): one
+// symbolic pass, then numeric passes as the values change.  Every numeric
+// pass of the reference re-derives where each product lands in its C row by
+// probing the accumulator (engine.cpp:259-267).  With the structure fixed,
+// that slot is a function of the structure alone, so after the second numeric
+// pass on a handle the slot of every product is recorded once:
+//
+//   slot map      one byte (rows <= 256 entries) or two bytes per product, in
+//                 the product order of the Thread-Sequential walk (A entry p,
+//                 then B-row entry t) — the order of the row's flops;
+//   column cache  C's column indices in first-touch order (4 B per entry).
+//
+// Later passes run replay_numeric_kernel: per product one map byte, one B
+// value and an unfused multiply + add onto acc[slot] in shared memory — no
+// key loads, probes or claims.  The first product of a slot lands on -0.0
+// (-0.0 + v == v bitwise, including v = +0.0 and NaN payloads) and the rest
+// are added in product order, so values are bitwise those of the hashing
+// kernels (and of the reference's raw output).
+//
+// The map is valid only for the structure it was recorded on.  The reference
+// checks dimensions and nnz only (engine.cpp:451-453); the replay path also
+// fingerprints A's and B's row offsets and column indices (a 64-bit
+// order-independent hash, relative to the row-offset base so row-block views
+// fingerprint like the matrix they were cut from) on every pass and falls
+// back to the hashing kernels when it differs.
+#include <cstdint>
+
+#include "kk_device.cuh"
+#include "kk_internal.h"
+
+namespace kk {
+
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x)
+{
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+__device__ __forceinline__ uint64_t fp_term(uint64_t salt, int64_t idx, int64_t value)
+{
+    return mix64(mix64(static_cast<uint64_t>(idx) * 0x9E3779B97F4A7C15ull + salt) ^ static_cast<uint64_t>(value));
+}
+
+// sum over (i, rowptr[i] - rowptr[0]) and (q, cols[rowptr[0] + q]) of fp_term
+__global__ void __launch_bounds__(256) fingerprint_kernel(int64_t rows, const int64_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ cols, uint64_t salt,
+                                                          unsigned long long* out)
+{
+    const int64_t base = __ldg(rowptr);
+    const int64_t nnz = __ldg(rowptr + rows) - base;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    uint64_t acc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows; i += stride)
+        acc += fp_term(salt, i, __ldg(rowptr + i) - base);
+    const uint64_t csalt = salt ^ 0x5bd1e9955bd1e995ull;
+    // cols: four per thread per iteration (int4 when 16-byte aligned)
+    const int32_t* c = cols + base;
+    const int64_t head = (reinterpret_cast<uintptr_t>(c) & 15) ? ((16 - (reinterpret_cast<uintptr_t>(c) & 15)) >> 2) : 0;
+    const int64_t h = head < nnz ? head : nnz;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < h; q += stride)
+        acc += fp_term(csalt, q, __ldg(c + q));
+    const int64_t nvec = (nnz - h) >> 2;
+    const int4* v = reinterpret_cast<const int4*>(c + h);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nvec; q += stride) {
+        const int4 x = __ldg(v + q);
+        const int64_t q0 = h + 4 * q;
+        acc += fp_term(csalt, q0, x.x) + fp_term(csalt, q0 + 1, x.y) + fp_term(csalt, q0 + 2, x.z)
+            + fp_term(csalt, q0 + 3, x.w);
+    }
+    for (int64_t q = h + 4 * nvec + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += stride)
+        acc += fp_term(csalt, q, __ldg(c + q));
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+        acc += __shfl_xor_sync(kFull, acc, off);
+    if ((threadIdx.x & 31) == 0)
+        atomicAdd(out, static_cast<unsigned long long>(acc));
+}
+
+struct StepStageR {
+    longlong2 row[32]; // x = B row offset, y = B row length
+    double a[32];
+};
+
+// Record each product's slot: the C row's first-touch columns go into a
+// per-warp hash (column -> position), then the row's products are walked in
+// Thread-Sequential order and looked up.  Also fills the column cache.
+template <typename PosT>
+__global__ void __launch_bounds__(256) replay_build_kernel(const ReplayLaunch R)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    int32_t* keys = reinterpret_cast<int32_t*>(smem + (size_t)wib * R.warp_bytes);
+    int32_t* posv = keys + R.T;
+    const uint32_t tmask = static_cast<uint32_t>(R.T - 1);
+    for (int t = lane; t < R.T; t += 32)
+        keys[t] = kEmpty;
+    __syncwarp();
+    PosT* map = static_cast<PosT*>(R.map);
+    const int64_t nwarps = (int64_t)gridDim.x * R.wpb;
+    for (int64_t i = (int64_t)blockIdx.x * R.wpb + wib; i < R.m; i += nwarps) {
+        const int64_t cbase = __ldg(R.c_rowptr + i);
+        const int32_t cap = static_cast<int32_t>(__ldg(R.c_rowptr + i + 1) - cbase);
+        if (cap == 0)
+            continue;
+        for (int32_t q = lane; q < cap; q += 32) {
+            const int32_t key = R.c_cols[cbase + q];
+            R.ccache[cbase + q] = key;
+            uint32_t s = hash_slot(key, R.shift);
+            while (atomicCAS(&keys[s], kEmpty, key) != kEmpty)
+                s = (s + 1) & tmask;
+            posv[s] = q;
+        }
+        __syncwarp();
+        int64_t poff = __ldg(R.prod_off + i);
+        const int64_t abeg = __ldg(R.a_rowptr + i), aend = __ldg(R.a_rowptr + i + 1);
+        for (int64_t p = abeg; p < aend; ++p) {
+            const int32_t j = __ldg(R.a_cols + p);
+            const int64_t b0 = __ldg(R.b_rowptr + j);
+            const int64_t len = __ldg(R.b_rowptr + j + 1) - b0;
+            for (int64_t t = lane; t < len; t += 32) {
+                const int32_t key = __ldg(R.b_cols + b0 + t);
+                uint32_t s = hash_slot(key, R.shift);
+                int32_t k = keys[s];
+                int probes = 0;
+                while (k != key && k != kEmpty && probes++ < R.T) {
+                    s = (s + 1) & tmask;
+                    k = keys[s];
+                }
+                PosT pos = 0;
+                if (k == key)
+                    pos = static_cast<PosT>(posv[s]);
+                else
+                    raise_error(R.ctr, kDevReplay);
+                map[poff + t] = pos;
+            }
+            poff += len;
+        }
+        __syncwarp();
+        for (int32_t q = lane; q < cap; q += 32) {
+            const int32_t key = R.c_cols[cbase + q];
+            uint32_t s = hash_slot(key, R.shift);
+            while (keys[s] != key)
+                s = (s + 1) & tmask;
+            keys[s] = kEmpty;
+        }
+        __syncwarp();
+    }
+}
+
+// Replay: warp per C row, Thread-Sequential steps (one B row per step, lanes
+// over its entries, so slots within a step are distinct), depth-2 register
+// prefetch of (slot, B value) like numeric_lp_seq_kernel.
+template <typename PosT>
+__global__ void __launch_bounds__(256) replay_numeric_kernel(const ReplayLaunch R)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    unsigned char* region = smem + (size_t)wib * R.warp_bytes;
+    StepStageR* stage = reinterpret_cast<StepStageR*>(region);
+    double* acc = reinterpret_cast<double*>(region + sizeof(StepStageR));
+    const PosT* __restrict__ map = static_cast<const PosT*>(R.map);
+    const double* __restrict__ b_vals = R.b_vals;
+    const int64_t nwarps = (int64_t)gridDim.x * R.wpb;
+    for (int64_t i = (int64_t)blockIdx.x * R.wpb + wib; i < R.m; i += nwarps) {
+        const int64_t cbase = __ldg(R.c_rowptr + i);
+        const int32_t cap = static_cast<int32_t>(__ldg(R.c_rowptr + i + 1) - cbase);
+        if (cap == 0)
+            continue;
+        for (int32_t q = lane; q < cap; q += 32)
+            acc[q] = -0.0;
+        int64_t poff = __ldg(R.prod_off + i);
+        const int64_t abeg = __ldg(R.a_rowptr + i), aend = __ldg(R.a_rowptr + i + 1);
+        bool bad = false;
+        for (int64_t p0 = abeg; p0 < aend; p0 += 32) {
+            const int na = static_cast<int>(aend - p0 < 32 ? aend - p0 : 32);
+            int32_t bl = 0;
+            if (lane < na) {
+                const int32_t j = __ldg(R.a_cols + p0 + lane);
+                const int64_t b0 = __ldg(R.b_rowptr + j);
+                bl = static_cast<int32_t>(__ldg(R.b_rowptr + j + 1) - b0);
+                stage->row[lane] = make_longlong2(b0, bl);
+                stage->a[lane] = __ldg(R.a_vals + p0 + lane);
+            } else {
+                stage->row[lane] = make_longlong2(0, 0);
+            }
+            const bool long_rows = __any_sync(kFull, bl > 32);
+            __syncwarp();
+            if (long_rows) {
+                for (int q = 0; q < na; ++q) {
+                    const longlong2 rq = stage->row[q];
+                    const double a = stage->a[q];
+                    for (int64_t t = lane; t < rq.y; t += 32) {
+                        const int32_t s = static_cast<int32_t>(__ldg(map + poff + t));
+                        const double v = __dmul_rn(a, __ldg(b_vals + rq.x + t));
+                        if (s < cap)
+                            acc[s] = __dadd_rn(acc[s], v);
+                        else
+                            bad = true;
+                    }
+                    poff += rq.y;
+                    __syncwarp();
+                }
+                continue;
+            }
+            // depth-2 pipeline; rows of the stage past na have length 0
+            int32_t s0 = 0, s1 = 0, len0, len1;
+            double v0 = 0.0, v1 = 0.0;
+            int64_t o1, o2;
+            {
+                const longlong2 r0 = stage->row[0];
+                const longlong2 r1 = stage->row[1];
+                len0 = static_cast<int32_t>(r0.y);
+                len1 = static_cast<int32_t>(r1.y);
+                o1 = poff + len0;
+                o2 = o1 + len1;
+                if (lane < len0) {
+                    s0 = __ldg(map + poff + lane);
+                    v0 = __ldg(b_vals + r0.x + lane);
+                }
+                if (lane < len1) {
+                    s1 = __ldg(map + o1 + lane);
+                    v1 = __ldg(b_vals + r1.x + lane);
+                }
+            }
+            for (int q = 0; q < na; ++q) {
+                int32_t s2 = 0, len2 = 0;
+                double v2 = 0.0;
+                if (q + 2 < 32) {
+                    const longlong2 r2 = stage->row[q + 2];
+                    len2 = static_cast<int32_t>(r2.y);
+                    if (lane < len2) {
+                        s2 = __ldg(map + o2 + lane);
+                        v2 = __ldg(b_vals + r2.x + lane);
+                    }
+                }
+                if (lane < len0) {
+                    const double v = __dmul_rn(stage->a[q], v0);
+                    if (s0 < cap)
+                        acc[s0] = __dadd_rn(acc[s0], v);
+                    else
+                        bad = true;
+                }
+                __syncwarp();
+                s0 = s1;
+                v0 = v1;
+                len0 = len1;
+                s1 = s2;
+                v1 = v2;
+                len1 = len2;
+                o2 += len2;
+            }
+            {
+                // products of this chunk: sum of the staged lengths
+                int32_t tot = bl;
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1)
+                    tot += __shfl_xor_sync(kFull, tot, off);
+                poff += tot;
+            }
+            __syncwarp();
+        }
+        if (__any_sync(kFull, bad) && lane == 0)
+            raise_error(R.ctr, kDevReplay);
+        for (int32_t q = lane; q < cap; q += 32) {
+            R.c_cols[cbase + q] = __ldg(R.ccache + cbase + q);
+            R.c_vals[cbase + q] = acc[q];
+        }
+        __syncwarp();
+    }
+}
+
+template <typename K>
+int blocks_per_sm(K kernel, int threads, size_t smem)
+{
+    const void* fn = reinterpret_cast<const void*>(kernel);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess)
+        return 1;
+    return b > 0 ? b : 1;
+}
+
+template <typename K>
+cudaError_t launch_rows(K kernel, ReplayLaunch R, cudaStream_t st)
+{
+    if (R.m <= 0)
+        return cudaSuccess;
+    const size_t smem = (size_t)R.wpb * R.warp_bytes;
+    const int per_sm = blocks_per_sm(kernel, R.wpb * 32, smem);
+    const int64_t want = (R.m + R.wpb - 1) / R.wpb;
+    const int64_t fit = (int64_t)per_sm * sm_count();
+    const int grid = static_cast<int>(want < fit ? want : fit);
+    kernel<<<grid, R.wpb * 32, smem, st>>>(R);
+    count_launch();
+    return cudaGetLastError();
+}
+
+} // namespace
+
+cudaError_t launch_fingerprint(int64_t rows, const int64_t* rowptr, const int32_t* cols, uint64_t salt,
+                               unsigned long long* out, cudaStream_t st)
+{
+    const int grid = sm_count() * 4;
+    fingerprint_kernel<<<grid, 256, 0, st>>>(rows, rowptr, cols, salt, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_replay_build(ReplayLaunch R, int width, cudaStream_t st)
+{
+    R.warp_bytes = 8ull * R.T; // keys[T] + positions[T]
+    R.wpb = static_cast<int>(R.warp_bytes >= 12288 ? 1 : 98304 / R.warp_bytes < 8 ? 98304 / R.warp_bytes : 8);
+    return width == 1 ? launch_rows(replay_build_kernel<uint8_t>, R, st)
+                      : launch_rows(replay_build_kernel<uint16_t>, R, st);
+}
+
+cudaError_t launch_replay_numeric(ReplayLaunch R, int width, int32_t max_row, cudaStream_t st)
+{
+    R.wpb = 8;
+    R.warp_bytes = (sizeof(StepStageR) + 8ull * (max_row > 0 ? max_row : 1) + 15) & ~15ull;
+    return width == 1 ? launch_rows(replay_numeric_kernel<uint8_t>, R, st)
+                      : launch_rows(replay_numeric_kernel<uint16_t>, R, st);
+}
+
+} // namespace kk

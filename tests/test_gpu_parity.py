@@ -219,6 +219,82 @@ def test_structure_mismatch_is_reported_not_hung(kk):
             kk.numeric(a, b2, h, kk.PhaseStats())
 
 
+def _scaled(kk, x, f):
+    return kk.CsrMatrix(x.num_rows, x.num_cols, x.row_offsets, x.col_indices, x.values * f, x.sorted_rows)
+
+
+@pytest.mark.parametrize("shape", [(300, 300, 300, 0.08), (120, 2000, 400, 0.03)])
+@pytest.mark.parametrize("sort", [False, True])
+def test_replay_passes_bitwise(kk, oracle, shape, sort):
+    """Structure reuse (engine.hpp:42-56): pass 2 records the slot map, passes
+    3+ replay it (kk_replay.cu); every pass must equal a fresh multiply bit
+    for bit.  Shapes give 1-byte (rows <= 256) and 2-byte slots."""
+    m, n, k, d = shape
+    rng = np.random.default_rng(int(1e6 * d) + m)
+    a = random_csr(rng, m, n, d, shuffle=True)
+    b = random_csr(rng, n, k, d * 3 if n > 1000 else d, shuffle=True)
+    cfg = kk.SpgemmConfig(sort_output=sort)
+    h = kk.symbolic(a, b, cfg)
+    assert h.replay_state == 1, "Thread-Sequential plan with warp-table rows must be replay-eligible"
+    if m == 120:
+        assert h.max_row_size > 256
+    for p in range(6):
+        ap, bp = _scaled(kk, a, 1.0 + 0.125 * p), _scaled(kk, b, 1.0 - 0.0625 * p)
+        st = kk.PhaseStats()
+        c = kk.numeric(ap, bp, h, st).to_host()
+        assert h.replay_state == (1 if p == 0 else 2)
+        fresh = kk.multiply(ap, bp, cfg).c.to_host()
+        assert np.array_equal(c.row_offsets, fresh.row_offsets)
+        assert np.array_equal(c.col_indices, fresh.col_indices)
+        assert np.array_equal(c.values.view(np.int64), fresh.values.view(np.int64))
+        if not sort:
+            assert_parity(oracle, ap, bp, c)
+
+
+def test_replay_falls_back_on_structure_change(kk, oracle):
+    rng = np.random.default_rng(23)
+    a = random_csr(rng, 200, 200, 0.1)
+    b = random_csr(rng, 200, 200, 0.1)
+    h = kk.symbolic(a, b)
+    for _ in range(3):
+        kk.numeric(a, b, h)
+    assert h.replay_state == 2
+    # same nnz, same row lengths, permuted columns inside B's rows: C's
+    # structure (and first-touch order) changes, so the map must not be used
+    b2 = kk.CsrMatrix(b.num_rows, b.num_cols, b.row_offsets, b.col_indices.copy(), b.values, False)
+    for i in range(b2.num_rows):
+        lo, hi = b2.row_offsets[i], b2.row_offsets[i + 1]
+        b2.col_indices[lo:hi] = b2.col_indices[lo:hi][::-1]
+    c2 = kk.numeric(a, b2, h, kk.PhaseStats()).to_host()  # same column sets: a valid reuse
+    assert_parity(oracle, a, b2, c2)
+    c = kk.numeric(a, b, h).to_host()
+    assert_parity(oracle, a, b, c)
+    # same nnz, different column sets: the hashing kernels report the mismatch
+    b3 = kk.CsrMatrix(b.num_rows, b.num_cols, b.row_offsets, b.col_indices.copy(), b.values, False)
+    for i in range(b3.num_rows):
+        lo, hi = b3.row_offsets[i], b3.row_offsets[i + 1]
+        b3.col_indices[lo:hi] = np.arange(hi - lo) % b3.num_cols
+    with pytest.raises(kk.InternalError):
+        kk.numeric(a, b3, h, kk.PhaseStats())
+
+
+def test_replay_row_block_views(kk, oracle):
+    rng = np.random.default_rng(29)
+    a = random_csr(rng, 400, 150, 0.12)
+    b = random_csr(rng, 150, 160, 0.12)
+    da, db = a.to_device(), b.to_device()
+    ro = oracle.symbolic_row_offsets(a, b)
+    full_cols, full_vals = oracle.numeric(a, b, ro)
+    lo, hi = 133, 311
+    blk = da.row_block(lo, hi)
+    h = kk.symbolic(blk, db)
+    for _ in range(4):
+        c = kk.numeric(blk, db, h).to_host()
+        assert np.array_equal(c.col_indices, full_cols[ro[lo]:ro[hi]])
+        assert np.array_equal(c.values.view(np.int64), full_vals[ro[lo]:ro[hi]].view(np.int64))
+    assert h.replay_state == 2
+
+
 def test_contract_errors(kk):
     a = csr_from_triplets(2, 3, [])
     b = csr_from_triplets(2, 2, [])
