@@ -186,6 +186,15 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg, spg_
 int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_cols,
                 double* c_vals, spg_phase_stats* stats, void* stream);
 
+/* numeric restricted to C rows [row_begin, row_end) (extension, no reference
+ * counterpart): same buffers and contract as spg_numeric, entries of other
+ * rows untouched.  Lets a host caller copy finished row blocks of C out while
+ * later blocks compute (paper_1801_03065_b200/host.py).  Only full-range
+ * passes count toward recording the slot replay. */
+int spg_numeric_rows(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t row_begin,
+                     int32_t row_end, int32_t* c_cols, double* c_vals, spg_phase_stats* stats,
+                     void* stream);
+
 /* Query / mutate / rebuild handles. */
 int spg_handle_info_get(spg_handle_t h, spg_handle_info* out);
 int spg_handle_copy_row_offsets(spg_handle_t h, int64_t* host_dst);

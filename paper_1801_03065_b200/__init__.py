@@ -158,7 +158,7 @@ EXPORTED_SYMBOLS = (
     "spg_symbolic", "spg_numeric", "spg_handle_info_get", "spg_handle_copy_row_offsets",
     "spg_handle_copy_per_row_flops", "spg_handle_copy_row_offsets_device", "spg_handle_set_numeric", "spg_handle_import",
     "spg_handle_check", "spg_handle_destroy", "spg_sort_rows", "spg_kernel_launch_count",
-    "spg_row_flops", "spg_handle_replay_state",
+    "spg_row_flops", "spg_handle_replay_state", "spg_numeric_rows",
 )
 
 _lib_handle = None
@@ -186,6 +186,9 @@ def lib() -> C.CDLL:
                                    C.POINTER(C.c_void_p), C.c_void_p]
         L.spg_numeric.argtypes = [C.c_void_p, C.POINTER(_Csr), C.POINTER(_Csr), C.c_void_p,
                                   C.c_void_p, C.POINTER(_PhaseStats), C.c_void_p]
+        L.spg_numeric_rows.restype = C.c_int
+        L.spg_numeric_rows.argtypes = [C.c_void_p, C.POINTER(_Csr), C.POINTER(_Csr), C.c_int32, C.c_int32,
+                                       C.c_void_p, C.c_void_p, C.POINTER(_PhaseStats), C.c_void_p]
         L.spg_handle_info_get.argtypes = [C.c_void_p, C.POINTER(_Info)]
         L.spg_handle_copy_row_offsets.argtypes = [C.c_void_p, C.c_void_p]
         L.spg_handle_copy_per_row_flops.argtypes = [C.c_void_p, C.c_void_p]
@@ -544,6 +547,22 @@ def numeric(a, b, handle: SpgemmHandle, stats: Optional[PhaseStats] = None, stre
     rowptr = handle.device_row_offsets(stream)
     return DeviceCsr(info.m, info.k, rowptr, cols[:nnz] if nnz else cols[:0],
                      vals[:nnz] if nnz else vals[:0], bool(info.config.sort_output), nnz)
+
+
+def numeric_rows(a, b, handle: SpgemmHandle, row_begin: int, row_end: int, cols, vals,
+                 stats: Optional[PhaseStats] = None, stream=None) -> None:
+    """numeric restricted to C rows [row_begin, row_end), into the full C
+    buffers `cols`/`vals` (nnz_c entries each; other rows untouched)."""
+    info = handle._info()
+    if a.num_rows != info.m or a.num_cols != info.n or b.num_rows != info.n or b.num_cols != info.k:
+        raise ReuseError("numeric: operands do not match the symbolic handle")
+    da, db = _dev(a), _dev(b)
+    st = _PhaseStats()
+    _check(lib().spg_numeric_rows(handle._ptr, C.byref(da._c()), C.byref(db._c()), row_begin, row_end,
+                                  cols.data_ptr(), vals.data_ptr(), C.byref(st) if stats is not None else None,
+                                  _stream_ptr(stream)))
+    if stats is not None:
+        stats.ms, stats.pool_allocations, stats.l2_inserts = st.ms, st.pool_allocations, st.l2_inserts
 
 
 def multiply(a, b, cfg: Optional[SpgemmConfig] = None, stream=None) -> MultiplyResult:

@@ -624,6 +624,8 @@ ReplayLaunch replay_launch(spg_handle* h, const spg_csr* a, const spg_csr* b, in
     R.map = h->d_map;
     R.prod_off = h->d_prod_off;
     R.m = h->info.m;
+    R.row_lo = 0;
+    R.row_hi = h->info.m;
     R.ctr = h->d_ctr;
     return R;
 }
@@ -1032,8 +1034,8 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
     return rc;
 }
 
-int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_cols, double* c_vals,
-                spg_phase_stats* stats, void* stream)
+static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t row_lo, int32_t row_hi,
+                        int32_t* c_cols, double* c_vals, spg_phase_stats* stats, void* stream)
 {
     return guarded([&] {
         if (!h)
@@ -1047,6 +1049,9 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
             fail(SPG_ERR_REUSE, "numeric: operands do not match the symbolic handle");
         if (I.nnz_c > 0 && (!c_cols || !c_vals))
             fail(SPG_ERR_CONTRACT, "numeric: null output buffers");
+        if (row_lo < 0 || row_hi > I.m || row_lo > row_hi)
+            fail(SPG_ERR_CONTRACT, "numeric: bad row range");
+        const bool full = row_lo == 0 && row_hi == I.m;
         require_device();
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         h->stream = st;
@@ -1058,13 +1063,16 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
         }
         cuda_check(cudaMemsetAsync(h->d_ctr, 0, sizeof(DevCounters), st), "memset");
         const PhasePlan& P = h->num;
-        ++h->numeric_calls;
+        if (full)
+            ++h->numeric_calls;
         bool replayed = false;
         if (h->replay_ready) {
             replay_fingerprints(h, a, b, st);
             if (h->h_fp[0] == h->fp_a && h->h_fp[1] == h->fp_b) {
-                cuda_check(launch_replay_numeric(replay_launch(h, a, b, c_cols, c_vals), h->replay_width,
-                                                 static_cast<int32_t>(I.max_row_size), st),
+                ReplayLaunch R = replay_launch(h, a, b, c_cols, c_vals);
+                R.row_lo = row_lo;
+                R.row_hi = row_hi;
+                cuda_check(launch_replay_numeric(R, h->replay_width, static_cast<int32_t>(I.max_row_size), st),
                            "replay numeric");
                 replayed = true;
             }
@@ -1083,6 +1091,10 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
             L.b_vals = b->values;
             L.list = P.need_list ? h->d_num_list + pc.off : nullptr;
             L.nrows = P.need_list ? pc.count : I.m;
+            L.row_lo = full ? 0 : row_lo;
+            L.row_hi = full ? 0 : row_hi;
+            if (!full && row_lo == row_hi)
+                break;
             L.c_rowptr = h->d_rowptr;
             L.c_cols = c_cols;
             L.c_vals = c_vals;
@@ -1118,10 +1130,11 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
                 cuda_check(launch_row_kernel(L, P.acc, P.flat, kVarNumeric, st), "numeric kernel");
             }
         }
-        if (!replayed && h->replay_eligible && !h->replay_ready && h->numeric_calls >= 2)
+        if (full && !replayed && h->replay_eligible && !h->replay_ready && h->numeric_calls >= 2)
             record_replay(h, a, b, c_cols, c_vals, st);
-        if (I.config.sort_output)
-            cuda_check(launch_sort_rows(I.m, h->d_rowptr, c_cols, c_vals, I.max_row_size, st), "sort_output");
+        if (I.config.sort_output && row_hi > row_lo)
+            cuda_check(launch_sort_rows(row_hi - row_lo, h->d_rowptr + row_lo, c_cols, c_vals, I.max_row_size, st),
+                       "sort_output");
         if (stats) {
             DevCounters hc{};
             cuda_check(cudaEventRecord(e1, st), "event");
@@ -1138,6 +1151,22 @@ int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_c
                 fail(SPG_ERR_INTERNAL, std::string("numeric: ") + dev_error_text(hc.error));
         }
     });
+}
+
+int spg_numeric(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t* c_cols, double* c_vals,
+                spg_phase_stats* stats, void* stream)
+{
+    if (!h)
+        return guarded([&] { fail(SPG_ERR_CONTRACT, "numeric: null handle"); });
+    return numeric_impl(h, a, b, 0, h->info.m, c_cols, c_vals, stats, stream);
+}
+
+int spg_numeric_rows(spg_handle_t h, const spg_csr* a, const spg_csr* b, int32_t row_begin, int32_t row_end,
+                     int32_t* c_cols, double* c_vals, spg_phase_stats* stats, void* stream)
+{
+    if (!h)
+        return guarded([&] { fail(SPG_ERR_CONTRACT, "numeric: null handle"); });
+    return numeric_impl(h, a, b, row_begin, row_end, c_cols, c_vals, stats, stream);
 }
 
 int spg_handle_info_get(spg_handle_t h, spg_handle_info* out)

@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
 
     for (int64_t r = (int64_t)blockIdx.x * L.wpb + wib; r < L.nrows; r += nwarps) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        if (L.row_hi > 0 && (i < L.row_lo || i >= L.row_hi))
+            continue; // outside the requested row range (spg_numeric_rows)
         const int64_t cbase = __ldg(L.c_rowptr + i);
         const int32_t cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
         if (cap == 0)
@@ -367,6 +369,8 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
 
     for (int64_t r = (int64_t)blockIdx.x * L.wpb + wib; r < L.nrows; r += nwarps) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        if (L.row_hi > 0 && (i < L.row_lo || i >= L.row_hi))
+            continue; // outside the requested row range (spg_numeric_rows)
         const int64_t cbase = __ldg(L.c_rowptr + i);
         const int32_t cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
         if (cap == 0)

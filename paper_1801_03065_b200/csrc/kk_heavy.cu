@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
 
     for (int64_t r = blockIdx.x; r < L.nrows; r += gridDim.x) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        if (L.row_hi > 0 && (i < L.row_lo || i >= L.row_hi))
+            continue; // outside the requested row range (spg_numeric_rows)
         const int64_t cbase = __ldg(L.c_rowptr + i);
         const int32_t cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
         const int64_t abeg = __ldg(L.a_rowptr + i), aend = __ldg(L.a_rowptr + i + 1);

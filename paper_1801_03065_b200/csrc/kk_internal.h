@@ -60,6 +60,7 @@ struct RowLaunch {
     // rows
     const int32_t* list; // nullptr: rows [0, nrows)
     int64_t nrows;
+    int32_t row_lo, row_hi; // numeric: only rows in [row_lo, row_hi) when row_hi > 0
     // outputs
     int64_t* sym_sizes;          // symbolic: sizes[i] (== rowptr + 1)
     const int64_t* c_rowptr;     // numeric
@@ -128,6 +129,7 @@ struct ReplayLaunch {
     void* map;                // uint8_t / uint16_t slot per product
     const int64_t* prod_off;  // [m+1] first product of each row
     int64_t m;
+    int32_t row_lo, row_hi;   // rows [row_lo, row_hi) (replay numeric)
     DevCounters* ctr;
     int32_t T;                // build: per-warp hash size (pow2 >= 2 * max row)
     int shift;                // build: 32 - log2(T)

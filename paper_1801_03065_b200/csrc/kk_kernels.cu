@@ -479,6 +479,8 @@ __global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
     unsigned long long my_alloc = 0, my_inserts = 0;
     for (int64_t r = gw; r < L.nrows; r += nwarps) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        if (L.row_hi > 0 && (i < L.row_lo || i >= L.row_hi))
+            continue; // outside the requested row range (spg_numeric_rows)
         int chunk = -1;
         if constexpr (kL2) {
             if (L.pool.mode != 0) {

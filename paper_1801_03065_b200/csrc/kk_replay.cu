@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) replay_numeric_kernel(const ReplayLaunch 
     const PosT* __restrict__ map = static_cast<const PosT*>(R.map);
     const double* __restrict__ b_vals = R.b_vals;
     const int64_t nwarps = (int64_t)gridDim.x * R.wpb;
-    for (int64_t i = (int64_t)blockIdx.x * R.wpb + wib; i < R.m; i += nwarps) {
+    for (int64_t i = R.row_lo + (int64_t)blockIdx.x * R.wpb + wib; i < R.row_hi; i += nwarps) {
         const int64_t cbase = __ldg(R.c_rowptr + i);
         const int32_t cap = static_cast<int32_t>(__ldg(R.c_rowptr + i + 1) - cbase);
         if (cap == 0)
@@ -292,13 +292,13 @@ int blocks_per_sm(K kernel, int threads, size_t smem)
 }
 
 template <typename K>
-cudaError_t launch_rows(K kernel, ReplayLaunch R, cudaStream_t st)
+cudaError_t launch_rows(K kernel, ReplayLaunch R, int64_t rows, cudaStream_t st)
 {
-    if (R.m <= 0)
+    if (rows <= 0)
         return cudaSuccess;
     const size_t smem = (size_t)R.wpb * R.warp_bytes;
     const int per_sm = blocks_per_sm(kernel, R.wpb * 32, smem);
-    const int64_t want = (R.m + R.wpb - 1) / R.wpb;
+    const int64_t want = (rows + R.wpb - 1) / R.wpb;
     const int64_t fit = (int64_t)per_sm * sm_count();
     const int grid = static_cast<int>(want < fit ? want : fit);
     kernel<<<grid, R.wpb * 32, smem, st>>>(R);
@@ -321,16 +321,17 @@ cudaError_t launch_replay_build(ReplayLaunch R, int width, cudaStream_t st)
 {
     R.warp_bytes = 8ull * R.T; // keys[T] + positions[T]
     R.wpb = static_cast<int>(R.warp_bytes >= 12288 ? 1 : 98304 / R.warp_bytes < 8 ? 98304 / R.warp_bytes : 8);
-    return width == 1 ? launch_rows(replay_build_kernel<uint8_t>, R, st)
-                      : launch_rows(replay_build_kernel<uint16_t>, R, st);
+    return width == 1 ? launch_rows(replay_build_kernel<uint8_t>, R, R.m, st)
+                      : launch_rows(replay_build_kernel<uint16_t>, R, R.m, st);
 }
 
 cudaError_t launch_replay_numeric(ReplayLaunch R, int width, int32_t max_row, cudaStream_t st)
 {
     R.wpb = 8;
     R.warp_bytes = (sizeof(StepStageR) + 8ull * (max_row > 0 ? max_row : 1) + 15) & ~15ull;
-    return width == 1 ? launch_rows(replay_numeric_kernel<uint8_t>, R, st)
-                      : launch_rows(replay_numeric_kernel<uint16_t>, R, st);
+    const int64_t rows = R.row_hi - R.row_lo;
+    return width == 1 ? launch_rows(replay_numeric_kernel<uint8_t>, R, rows, st)
+                      : launch_rows(replay_numeric_kernel<uint16_t>, R, rows, st);
 }
 
 } // namespace kk

@@ -1,0 +1,195 @@
+"""Host-memory multiply with copy/compute overlap (the reference's
+`multiply(const CsrMatrix&, const CsrMatrix&, const SpgemmConfig&)`,
+engine.hpp:100-103, for callers whose matrices live in host memory).
+
+The reference is a CPU library: its multiply reads host CSR arrays and returns
+a host CSR.  On a B200 the end-to-end cost of that call is dominated by the
+host link (C is typically 4-5x larger than A), so the host path is organised
+around the copies:
+
+  * the operands' structure (row offsets, columns) is uploaded first and their
+    values on a second stream, overlapping the symbolic phase (which reads
+    structure only);
+  * a matrix passed as both A and B (C = A*A) is uploaded once; `a_rows`
+    names A as a row block of B (the row-sharded multi-GPU case) so only B
+    travels;
+  * one symbolic pass over all of A (C's size is then known and, unless the
+    caller passes output buffers, the pinned output comes from torch's host
+    caching allocator); the numeric pass then runs in row blocks
+    (spg_numeric_rows) and block k's C is copied out on the copy stream while
+    block k+1 computes.
+
+Inputs must be in pinned host memory (PinnedCsr) for the copies to be
+asynchronous.  Everything below the Python orchestration is the C ABI.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import CsrMatrix, DeviceCsr, SpgemmConfig, numeric_rows, symbolic
+
+_copy_streams = {}
+
+
+def _copy_stream(dev):
+    import torch
+    s = _copy_streams.get(dev.index)
+    if s is None:
+        s = torch.cuda.Stream(device=dev)
+        _copy_streams[dev.index] = s
+    return s
+
+
+@dataclasses.dataclass
+class PinnedCsr:
+    """A host CSR whose arrays are pinned torch tensors."""
+    num_rows: int
+    num_cols: int
+    row_offsets: "object"  # torch.int64 [num_rows+1], pinned
+    col_indices: "object"  # torch.int32, pinned
+    values: "object"       # torch.float64, pinned
+    sorted_rows: bool = False
+
+    @staticmethod
+    def from_csr(a: CsrMatrix) -> "PinnedCsr":
+        import torch
+
+        def pin(x, dt):
+            return torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).pin_memory()
+        base = int(a.row_offsets[0]) if len(a.row_offsets) else 0
+        n = a.nnz()
+        return PinnedCsr(a.num_rows, a.num_cols, pin(np.asarray(a.row_offsets) - base, np.int64),
+                         pin(a.col_indices[base:base + n], np.int32), pin(a.values[base:base + n], np.float64),
+                         a.sorted_rows)
+
+    def nnz(self) -> int:
+        return int(self.row_offsets[-1]) if self.row_offsets.numel() else 0
+
+    def nbytes(self) -> int:
+        return self.row_offsets.numel() * 8 + self.col_indices.numel() * 4 + self.values.numel() * 8
+
+
+@dataclasses.dataclass
+class HostResult:
+    """C in pinned host memory; `c` holds numpy views of the pinned tensors."""
+    c: CsrMatrix
+    h2d_bytes: int
+    d2h_bytes: int
+    blocks: int
+    _keep: Tuple = ()
+
+
+def _row_cuts(row_offsets: np.ndarray, lo: int, hi: int, blocks: int) -> List[int]:
+    """Row cut points of [lo, hi) balancing A's entries (a flop proxy that
+    needs no device pass)."""
+    if blocks <= 1 or hi - lo <= blocks:
+        return [lo, hi]
+    ro = row_offsets[lo:hi + 1]
+    targets = ro[0] + (ro[-1] - ro[0]) * np.arange(1, blocks) / blocks
+    inner = (np.searchsorted(ro, targets) + lo).tolist()
+    cuts = [lo] + [int(x) for x in inner] + [hi]
+    return sorted(set(cuts))
+
+
+def multiply_host(a: PinnedCsr, b: Optional[PinnedCsr] = None, cfg: Optional[SpgemmConfig] = None,
+                  a_rows: Optional[Tuple[int, int]] = None, blocks: Optional[int] = None,
+                  device=None, out: Optional[Tuple] = None, timeline: Optional[list] = None) -> HostResult:
+    """C = A*B from pinned host CSR to pinned host CSR.
+
+    b None (or b is a): C = A*A, uploaded once.  a_rows=(lo, hi): A is rows
+    [lo, hi) of B (a is ignored then), so only B is uploaded.  out = pinned
+    (row_offsets int64, col_indices int32, values float64) tensors to fill
+    when large enough (else C's arrays come from torch's pinned cache).
+    timeline: a list that receives (label, cuda event) marks."""
+    import torch
+
+    def mark(label, stream):
+        if timeline is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            timeline.append((label, ev))
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    main = torch.cuda.current_stream(dev)
+    side = _copy_stream(dev)
+    same = b is None or b is a
+    src_b = a if same else b
+    if a_rows is not None:
+        same = True
+        src_b = b if b is not None else a
+    lo, hi = a_rows if a_rows is not None else (0, (a if a is not None else src_b).num_rows)
+
+    # ---- uploads: structure on the main stream, values on the copy stream ----
+    def up_structure(x: PinnedCsr):
+        return (x.row_offsets.to(dev, non_blocking=True), x.col_indices.to(dev, non_blocking=True))
+
+    mark("start", main)
+    ro_b, ci_b = up_structure(src_b)
+    mark("structure uploaded", main)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        v_b = src_b.values.to(dev, non_blocking=True)
+    h2d = src_b.nbytes()
+    if not same:
+        ro_a, ci_a = up_structure(a)
+        with torch.cuda.stream(side):
+            v_a = a.values.to(dev, non_blocking=True)
+        h2d += a.nbytes()
+    values_ready = torch.cuda.Event()
+    values_ready.record(side)
+    mark("values uploaded", side)
+    dB = DeviceCsr(src_b.num_rows, src_b.num_cols, ro_b, ci_b, v_b, src_b.sorted_rows, src_b.nnz())
+    if same:
+        dA_full, a_host_ro = dB, src_b.row_offsets.numpy()
+    else:
+        dA_full = DeviceCsr(a.num_rows, a.num_cols, ro_a, ci_a, v_a, a.sorted_rows, a.nnz())
+        a_host_ro = a.row_offsets.numpy()
+
+    nnz_a = int(a_host_ro[hi] - a_host_ro[lo])
+    if blocks is None:
+        blocks = 1 if nnz_a < (1 << 22) else 8
+    cuts = _row_cuts(a_host_ro, lo, hi, blocks)
+
+    # ---- one symbolic over A's structure (overlaps the value upload) ----
+    dA = dA_full.row_block(lo, hi)
+    h = symbolic(dA, dB, cfg, stream=main)
+    nnz_c = h.nnz_c()
+    m = hi - lo
+    c_ro = h.device_row_offsets(main)
+    ro_host = h.c_row_offsets  # block boundaries of C (one small copy)
+    mark("symbolic done", main)
+    if out is not None and out[0].numel() >= m + 1 and out[1].numel() >= nnz_c and out[2].numel() >= nnz_c:
+        o_ro, o_ci, o_v = out
+    else:
+        o_ro = torch.empty(m + 1, dtype=torch.int64, pin_memory=True)
+        o_ci = torch.empty(max(nnz_c, 1), dtype=torch.int32, pin_memory=True)
+        o_v = torch.empty(max(nnz_c, 1), dtype=torch.float64, pin_memory=True)
+    d_ci = torch.empty(max(nnz_c, 1), dtype=torch.int32, device=dev)
+    d_v = torch.empty(max(nnz_c, 1), dtype=torch.float64, device=dev)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        o_ro[:m + 1].copy_(c_ro, non_blocking=True)
+
+    # ---- numeric per row block; block k's C copies out while block k+1 computes ----
+    main.wait_event(values_ready)
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        b0, b1 = r0 - lo, r1 - lo
+        numeric_rows(dA, dB, h, b0, b1, d_ci, d_v, stream=main)
+        done = torch.cuda.Event()
+        done.record(main)
+        side.wait_event(done)
+        e0, e1 = int(ro_host[b0]), int(ro_host[b1])
+        if e1 > e0:
+            with torch.cuda.stream(side):
+                o_ci[e0:e1].copy_(d_ci[e0:e1], non_blocking=True)
+                o_v[e0:e1].copy_(d_v[e0:e1], non_blocking=True)
+        mark(f"numeric {r0}:{r1}", main)
+        mark(f"copied {r0}:{r1}", side)
+    main.wait_stream(side)
+    main.synchronize()  # the reference's multiply returns a finished host CSR
+    sorted_c = bool(cfg.sort_output) if cfg is not None else False
+    c = CsrMatrix(m, src_b.num_cols, o_ro.numpy()[:m + 1], o_ci.numpy()[:nnz_c], o_v.numpy()[:nnz_c], sorted_c)
+    d2h = (m + 1) * 8 + nnz_c * 12
+    return HostResult(c, h2d, d2h, len(cuts) - 1, (o_ro, o_ci, o_v))

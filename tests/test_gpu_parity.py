@@ -472,3 +472,55 @@ def test_flop_balanced_shards_reassemble(kk, oracle, world):
     offs = shard.block_offsets(nnzs)
     assert offs == [int(ro[c]) for c in cuts]
     assert max(flops) - min(flops) <= 2 * 729  # lower_bound cuts: within two rows
+
+
+@pytest.mark.parametrize("blocks", [1, 3])
+def test_multiply_host_pipelined(kk, oracle, blocks):
+    """host.multiply_host (pinned host CSR in and out, row blocks overlapping
+    copies with compute) equals the device multiply bit for bit."""
+    from paper_1801_03065_b200 import host
+    rng = np.random.default_rng(31 + blocks)
+    a = random_csr(rng, 240, 240, 0.06)
+    b = random_csr(rng, 240, 180, 0.05)
+    pa, pb = host.PinnedCsr.from_csr(a), host.PinnedCsr.from_csr(b)
+    # A*B
+    r = host.multiply_host(pa, pb, blocks=blocks)
+    assert r.h2d_bytes == pa.nbytes() + pb.nbytes()
+    assert_parity(oracle, a, b, r.c)
+    # A*A, uploaded once
+    r2 = host.multiply_host(pa, blocks=blocks)
+    assert r2.h2d_bytes == pa.nbytes()
+    assert_parity(oracle, a, a, r2.c)
+    # rows [50, 190) of A times A: only A travels
+    r3 = host.multiply_host(None, pa, a_rows=(50, 190), blocks=blocks)
+    ro = oracle.symbolic_row_offsets(a, a)
+    cols, vals = oracle.numeric(a, a, ro)
+    assert np.array_equal(r3.c.row_offsets, ro[50:191] - ro[50])
+    assert np.array_equal(r3.c.col_indices, cols[ro[50]:ro[190]])
+    assert np.array_equal(r3.c.values.view(np.int64), vals[ro[50]:ro[190]].view(np.int64))
+
+
+@pytest.mark.parametrize("sort", [False, True])
+def test_numeric_rows_blocks_equal_full(kk, oracle, sort):
+    """spg_numeric_rows over a partition of the rows fills the same C as one
+    spg_numeric, before and after the slot replay is recorded."""
+    import torch
+    rng = np.random.default_rng(41 + sort)
+    a = random_csr(rng, 500, 300, 0.05)
+    b = random_csr(rng, 300, 400, 0.08)
+    cfg = kk.SpgemmConfig(sort_output=sort)
+    da, db = a.to_device(), b.to_device()
+    h = kk.symbolic(da, db, cfg)
+    full = kk.numeric(da, db, h).to_host()
+    for rep in range(3):  # pass 2 (rep 1) records the replay; 3 replays
+        kk.numeric(da, db, h)
+        nnz = h.nnz_c()
+        cols = torch.full((nnz,), -7, dtype=torch.int32, device="cuda")
+        vals = torch.zeros(nnz, dtype=torch.float64, device="cuda")
+        for r0, r1 in ((0, 0), (0, 123), (123, 124), (124, 400), (400, 500)):
+            kk.numeric_rows(da, db, h, r0, r1, cols, vals)
+        assert np.array_equal(cols.cpu().numpy(), full.col_indices)
+        assert np.array_equal(vals.cpu().numpy().view(np.int64), full.values.view(np.int64))
+    assert h.replay_state == 2
+    with pytest.raises(kk.ContractError):
+        kk.numeric_rows(da, db, h, 10, 5, cols, vals)
