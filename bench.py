@@ -391,7 +391,7 @@ def main():
                      "model": "16(m+1)+28nnzA+12flops+12nnzC (SURVEY §8d)"},
         "roofline_replay": None if replay_state != 2 else {
             "bound": "hbm", "achieved": replay_bytes / (replay_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-            "frac": replay_bytes / (replay_ms / 1e3) / 1e9 / hbm, "kernel": "replay_numeric_kernel (+2 fingerprints)",
+            "frac": replay_bytes / (replay_ms / 1e3) / 1e9 / hbm, "kernel": "replay_numeric_kernel (+ structure fingerprint pass)",
             "algorithmic_bytes": replay_bytes, "model": "24(m+1)+28nnzA+(8+w)flops+16nnzC, w = slot bytes"},
         "cpu_baseline": cpu,
         "e2e": e2e,

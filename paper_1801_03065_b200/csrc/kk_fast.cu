@@ -131,6 +131,8 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
     int32_t* keys = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
     int32_t* slot_of = reinterpret_cast<int32_t*>(region + L.lay.off_aux);
     StepStage* stage = reinterpret_cast<StepStage*>(region + L.lay.off_pay);
+    if (L.gate && L.gate[0] == L.gate[2] && L.gate[1] == L.gate[3])
+        return; // the slot replay (kk_replay.cu) computed this pass
     const uint32_t tmask = static_cast<uint32_t>(L.lay.T - 1);
     const int shift = L.lay.shift;
     for (int t = lane; t < L.lay.T; t += 32)
@@ -250,6 +252,15 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
 // inside the window form a bit mask M: lane x's segment is (segments started
 // before the window) + popc(M & lanes<=x) - 1.
 // ---------------------------------------------------------------------------
+// per-warp scratch for the compaction (shared memory, 640 B)
+struct FlatScratch {
+    int64_t base[32];
+    double a[32];
+    int32_t excl[32];
+};
+static_assert(sizeof(FlatScratch) == 640, "layouts reserve 640 B (symbolic) / 768 B (numeric)");
+
+template <bool kWithA>
 struct FlatMap {
     int64_t cbase;  // compacted: lane c holds the B-row base of the c-th non-empty segment
     double ca;      // ... its A value
@@ -258,7 +269,10 @@ struct FlatMap {
     int32_t rank;   // non-empty segments starting before the current window
     int32_t total;  // products of the chunk
 
-    __device__ __forceinline__ void init(int64_t bb, int32_t bl, double av, int lane)
+    // non-empty segments scatter their data to their rank in `sc` and every
+    // lane reads back entry `lane` (a shared-memory compaction: cheaper than
+    // locating the lane-th set bit of the mask)
+    __device__ __forceinline__ void init(int64_t bb, int32_t bl, double av, int lane, FlatScratch* sc)
     {
         int32_t incl = bl;
 #pragma unroll
@@ -271,10 +285,24 @@ struct FlatMap {
         total = __shfl_sync(kFull, incl, 31);
         const uint32_t ne = __ballot_sync(kFull, bl > 0);
         nne = __popc(ne);
-        const int src = lane < nne ? static_cast<int>(__fns(ne, 0, lane + 1)) : lane;
-        cbase = __shfl_sync(kFull, bb, src);
-        ca = __shfl_sync(kFull, av, src);
-        cexcl = __shfl_sync(kFull, excl, src);
+        if (bl > 0) {
+            const int r = __popc(ne & lanemask_lt());
+            sc->base[r] = bb;
+            sc->excl[r] = excl;
+            if constexpr (kWithA)
+                sc->a[r] = av;
+        }
+        __syncwarp();
+        cbase = 0;
+        ca = 0.0;
+        cexcl = 0;
+        if (lane < nne) {
+            cbase = sc->base[lane];
+            cexcl = sc->excl[lane];
+            if constexpr (kWithA)
+                ca = sc->a[lane];
+        }
+        __syncwarp();
         rank = 0;
     }
 
@@ -287,7 +315,8 @@ struct FlatMap {
         seg = seg < 0 ? 0 : (seg > 31 ? 31 : seg);
         e = __shfl_sync(kFull, cexcl, seg);
         base = __shfl_sync(kFull, cbase, seg);
-        a = __shfl_sync(kFull, ca, seg);
+        if constexpr (kWithA)
+            a = __shfl_sync(kFull, ca, seg);
         rank += __popc(M);
     }
 };
@@ -357,6 +386,7 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
     double* vals = reinterpret_cast<double*>(region + L.lay.off_map);
     int32_t* keys = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
     int32_t* slot_of = reinterpret_cast<int32_t*>(region + L.lay.off_aux);
+    FlatScratch* scratch = reinterpret_cast<FlatScratch*>(region + L.lay.off_pay);
     const uint32_t tmask = static_cast<uint32_t>(L.lay.T - 1);
     const int shift = L.lay.shift;
     for (int t = lane; t < L.lay.T; t += 32)
@@ -390,8 +420,8 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
             }
             // flattened prefix of this chunk's B-row lengths (32-bit: one
             // chunk of a flat-scheme row never holds 2^31 products)
-            FlatMap fm;
-            fm.init(bb, bl, av, lane);
+            FlatMap<true> fm;
+            fm.init(bb, bl, av, lane, scratch);
             const int32_t total = fm.total;
             for (int32_t w0 = 0; w0 < total; w0 += 32) {
                 const int32_t t = w0 + lane;
@@ -463,6 +493,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
     unsigned char* region = smem + (size_t)wib * L.lay.bytes;
     int32_t* keys = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
     uint32_t* words = reinterpret_cast<uint32_t*>(region + L.lay.off_map);
+    FlatScratch* scratch = reinterpret_cast<FlatScratch*>(region + L.lay.off_pay);
     const int T = L.lay.T;
     const uint32_t tmask = static_cast<uint32_t>(T - 1);
     const int pshift = L.lay.shift;
@@ -483,6 +514,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
         const int64_t abeg = __ldg(a_rowptr + i), aend = __ldg(a_rowptr + i + 1);
         int32_t used = 0; // claimed slots (warp-uniform after each window)
         bool overflow = false;
+        bool prev_claimed = false;
         for (int64_t p0 = abeg; p0 < aend && !overflow; p0 += 32) {
             const int na = static_cast<int>(aend - p0 < 32 ? aend - p0 : 32);
             int64_t bb = 0;
@@ -492,8 +524,8 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                 bb = __ldg(b_rowptr + j);
                 bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
             }
-            FlatMap fm;
-            fm.init(bb, bl, 0.0, lane);
+            FlatMap<false> fm;
+            fm.init(bb, bl, 0.0, lane, scratch);
             const int32_t total = fm.total;
             // window w0's (key, word) are loaded one window ahead
             auto fetch = [&](int32_t w0, int32_t& key, uint32_t& word) {
@@ -544,13 +576,19 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                     if constexpr (kCompressed)
                         atomicOr(&words[s], word);
                 }
-                used += __popc(__ballot_sync(kFull, claimed));
+                // claims are counted one window late (the ballot then never
+                // waits on this window's CAS); a table can fill up before the
+                // count sees it, but such a row is always flagged at its end
+                used += __popc(__ballot_sync(kFull, prev_claimed));
+                prev_claimed = claimed;
                 if (used > cap) { // table too small for this row: hand it to the L2 path
                     overflow = true;
                     break;
                 }
             }
         }
+        used += __popc(__ballot_sync(kFull, prev_claimed));
+        overflow = overflow || used > cap;
         __syncwarp();
         int64_t size = 0;
         for (int t = lane; t < T; t += 32) {

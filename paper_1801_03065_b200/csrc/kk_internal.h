@@ -61,6 +61,7 @@ struct RowLaunch {
     const int32_t* list; // nullptr: rows [0, nrows)
     int64_t nrows;
     int32_t row_lo, row_hi; // numeric: only rows in [row_lo, row_hi) when row_hi > 0
+    const unsigned long long* gate; // numeric fast kernel: exit when gate[0..1] == gate[2..3] (replayed)
     // outputs
     int64_t* sym_sizes;          // symbolic: sizes[i] (== rowptr + 1)
     const int64_t* c_rowptr;     // numeric
@@ -130,14 +131,15 @@ struct ReplayLaunch {
     const int64_t* prod_off;  // [m+1] first product of each row
     int64_t m;
     int32_t row_lo, row_hi;   // rows [row_lo, row_hi) (replay numeric)
+    const unsigned long long* gate; // run only when gate[0..1] == gate[2..3]
     DevCounters* ctr;
     int32_t T;                // build: per-warp hash size (pow2 >= 2 * max row)
     int shift;                // build: 32 - log2(T)
     int wpb;
     uint64_t warp_bytes;
 };
-cudaError_t launch_fingerprint(int64_t rows, const int64_t* rowptr, const int32_t* cols, uint64_t salt,
-                               unsigned long long* out, cudaStream_t st);
+cudaError_t launch_fingerprint(int64_t rows, const int64_t* rowptr, const int32_t* cols, unsigned long long* out0,
+                               unsigned long long* out1, cudaStream_t st);
 cudaError_t launch_replay_build(ReplayLaunch R, int width, cudaStream_t st);
 cudaError_t launch_replay_numeric(ReplayLaunch R, int width, int32_t max_row, cudaStream_t st);
 

@@ -21,10 +21,11 @@
 //
 // The map is valid only for the structure it was recorded on.  The reference
 // checks dimensions and nnz only (engine.cpp:451-453); the replay path also
-// fingerprints A's and B's row offsets and column indices (a 64-bit
-// order-independent hash, relative to the row-offset base so row-block views
-// fingerprint like the matrix they were cut from) on every pass and falls
-// back to the hashing kernels when it differs.
+// fingerprints A's and B's row offsets and column indices (64-bit,
+// position-weighted, relative to the row-offset base so row-block views
+// fingerprint like the matrix they were cut from) on every pass.  The replay
+// kernel and the hashing kernels are both launched and both read the
+// fingerprints: exactly one of them does the work, with no host round trip.
 #include <cstdint>
 
 #include "kk_device.cuh"
@@ -34,54 +35,59 @@ namespace kk {
 
 namespace {
 
-__device__ __forceinline__ uint64_t mix64(uint64_t x)
+// Position-weighted sum: element idx contributes value * (2K*idx + 1) (mod
+// 2^64).  The weights are odd, so any single changed entry changes the sum;
+// unrelated changes cancel with probability ~2^-64.  Weights advance by
+// additions only.
+constexpr uint64_t kFpK2 = 0x3C6EF372FE94F82Aull; // 2 * 0x9E3779B97F4A7C15 (mod 2^64)
+
+__device__ __forceinline__ uint64_t fp_weight(int64_t idx)
 {
-    x ^= x >> 30;
-    x *= 0xbf58476d1ce4e5b9ull;
-    x ^= x >> 27;
-    x *= 0x94d049bb133111ebull;
-    x ^= x >> 31;
-    return x;
+    return static_cast<uint64_t>(idx) * kFpK2 + 1ull;
 }
 
-__device__ __forceinline__ uint64_t fp_term(uint64_t salt, int64_t idx, int64_t value)
-{
-    return mix64(mix64(static_cast<uint64_t>(idx) * 0x9E3779B97F4A7C15ull + salt) ^ static_cast<uint64_t>(value));
-}
-
-// sum over (i, rowptr[i] - rowptr[0]) and (q, cols[rowptr[0] + q]) of fp_term
+// sum over (i, rowptr[i] - rowptr[0]) and (q, cols[rowptr[0] + q]); the row
+// offsets are weighted from index nnz + 1 on so they never share weights with
+// the columns.  Added into out0 (and out1 when A and B are the same arrays).
 __global__ void __launch_bounds__(256) fingerprint_kernel(int64_t rows, const int64_t* __restrict__ rowptr,
-                                                          const int32_t* __restrict__ cols, uint64_t salt,
-                                                          unsigned long long* out)
+                                                          const int32_t* __restrict__ cols,
+                                                          unsigned long long* out0, unsigned long long* out1)
 {
     const int64_t base = __ldg(rowptr);
     const int64_t nnz = __ldg(rowptr + rows) - base;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t acc = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows; i += stride)
-        acc += fp_term(salt, i, __ldg(rowptr + i) - base);
-    const uint64_t csalt = salt ^ 0x5bd1e9955bd1e995ull;
-    // cols: four per thread per iteration (int4 when 16-byte aligned)
+    for (int64_t i = tid; i <= rows; i += stride)
+        acc += static_cast<uint64_t>(__ldg(rowptr + i) - base) * fp_weight(nnz + 1 + i);
+    // columns: four per thread per iteration (int4 once 16-byte aligned)
     const int32_t* c = cols + base;
-    const int64_t head = (reinterpret_cast<uintptr_t>(c) & 15) ? ((16 - (reinterpret_cast<uintptr_t>(c) & 15)) >> 2) : 0;
+    const uintptr_t mis = reinterpret_cast<uintptr_t>(c) & 15;
+    const int64_t head = mis ? static_cast<int64_t>((16 - mis) >> 2) : 0;
     const int64_t h = head < nnz ? head : nnz;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < h; q += stride)
-        acc += fp_term(csalt, q, __ldg(c + q));
+    for (int64_t q = tid; q < h; q += stride)
+        acc += static_cast<uint64_t>(static_cast<uint32_t>(__ldg(c + q))) * fp_weight(q);
     const int64_t nvec = (nnz - h) >> 2;
     const int4* v = reinterpret_cast<const int4*>(c + h);
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nvec; q += stride) {
+    uint64_t w = fp_weight(h + 4 * tid);
+    const uint64_t wstep = 4ull * static_cast<uint64_t>(stride) * kFpK2;
+    for (int64_t q = tid; q < nvec; q += stride, w += wstep) {
         const int4 x = __ldg(v + q);
-        const int64_t q0 = h + 4 * q;
-        acc += fp_term(csalt, q0, x.x) + fp_term(csalt, q0 + 1, x.y) + fp_term(csalt, q0 + 2, x.z)
-            + fp_term(csalt, q0 + 3, x.w);
+        acc += static_cast<uint64_t>(static_cast<uint32_t>(x.x)) * w
+            + static_cast<uint64_t>(static_cast<uint32_t>(x.y)) * (w + kFpK2)
+            + static_cast<uint64_t>(static_cast<uint32_t>(x.z)) * (w + 2 * kFpK2)
+            + static_cast<uint64_t>(static_cast<uint32_t>(x.w)) * (w + 3 * kFpK2);
     }
-    for (int64_t q = h + 4 * nvec + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += stride)
-        acc += fp_term(csalt, q, __ldg(c + q));
+    for (int64_t q = h + 4 * nvec + tid; q < nnz; q += stride)
+        acc += static_cast<uint64_t>(static_cast<uint32_t>(__ldg(c + q))) * fp_weight(q);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1)
         acc += __shfl_xor_sync(kFull, acc, off);
-    if ((threadIdx.x & 31) == 0)
-        atomicAdd(out, static_cast<unsigned long long>(acc));
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out0, static_cast<unsigned long long>(acc));
+        if (out1)
+            atomicAdd(out1, static_cast<unsigned long long>(acc));
+    }
 }
 
 struct StepStageR {
@@ -168,6 +174,8 @@ __global__ void __launch_bounds__(256) replay_numeric_kernel(const ReplayLaunch 
     unsigned char* region = smem + (size_t)wib * R.warp_bytes;
     StepStageR* stage = reinterpret_cast<StepStageR*>(region);
     double* acc = reinterpret_cast<double*>(region + sizeof(StepStageR));
+    if (R.gate && !(R.gate[0] == R.gate[2] && R.gate[1] == R.gate[3]))
+        return; // structure changed since the map was recorded: the hashing kernels run
     const PosT* __restrict__ map = static_cast<const PosT*>(R.map);
     const double* __restrict__ b_vals = R.b_vals;
     const int64_t nwarps = (int64_t)gridDim.x * R.wpb;
@@ -308,11 +316,11 @@ cudaError_t launch_rows(K kernel, ReplayLaunch R, int64_t rows, cudaStream_t st)
 
 } // namespace
 
-cudaError_t launch_fingerprint(int64_t rows, const int64_t* rowptr, const int32_t* cols, uint64_t salt,
-                               unsigned long long* out, cudaStream_t st)
+cudaError_t launch_fingerprint(int64_t rows, const int64_t* rowptr, const int32_t* cols, unsigned long long* out0,
+                               unsigned long long* out1, cudaStream_t st)
 {
     const int grid = sm_count() * 4;
-    fingerprint_kernel<<<grid, 256, 0, st>>>(rows, rowptr, cols, salt, out);
+    fingerprint_kernel<<<grid, 256, 0, st>>>(rows, rowptr, cols, out0, out1);
     count_launch();
     return cudaGetLastError();
 }
