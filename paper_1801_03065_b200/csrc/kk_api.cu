@@ -111,8 +111,9 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kWarpSmemMax = 48 * 1024; // L1 accumulator budget per warp
 constexpr int32_t kHeavySymWords = 49152;     // 192 KB dense bitmap per CTA (heavy symbolic)
-constexpr int kHeavyLogW = 10;                // numeric heavy rows: 1024-column buckets
-constexpr int32_t kHeavyMaxBuckets = 1024;    // => k <= 2^20 for the bucketed numeric path
+constexpr int32_t kHeavyBucketKeys = 384;     // numeric heavy rows: ~distinct columns per hashed bucket
+constexpr int32_t kHeavyMaxBuckets = 1280;    // buckets per row (shared-memory histogram bound)
+constexpr int64_t kHeavyMaxRow = int64_t{kHeavyMaxBuckets} * 640; // <= 62.5% load of the 1024-slot tables
 constexpr uint64_t kCtaSmem = 96 * 1024;     // two CTAs per SM
 
 // device-side allocation helper (stream ordered)
@@ -572,15 +573,15 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
     }
     h->num = plan_phase(acc, flat, kVarNumeric, h->info.k, h->size_hist.hist, h->info.max_row_size, cfg, fast, 0);
     // Auto: rows beyond the warp tables take the bucketed CTA path (kk_heavy.cu)
-    // when the column domain has at most kHeavyMaxBuckets buckets and a row's
-    // products fit 32-bit staging offsets
+    // when a row's distinct columns fit the hashed buckets and its products
+    // fit 32-bit staging offsets
     h->num_heavy = false;
     if (fast && !forced && h->num.l2_class >= 0) {
-        const int64_t nb = (int64_t{h->info.k} + (1 << kHeavyLogW) - 1) >> kHeavyLogW;
         const int64_t cap = std::max<int64_t>(h->info.flops.max_row_flops, 1);
-        if (nb <= kHeavyMaxBuckets && cap < (int64_t{1} << 31)) {
+        if (h->info.max_row_size <= kHeavyMaxRow && cap < (int64_t{1} << 31)) {
             h->num_heavy = true;
-            h->heavy_nb = static_cast<int>(std::max<int64_t>(nb, 1));
+            h->heavy_nb = static_cast<int>(std::clamp<int64_t>(
+                (h->info.max_row_size + kHeavyBucketKeys - 1) / kHeavyBucketKeys, 1, kHeavyMaxBuckets));
             h->heavy_cap = cap;
         }
     }
@@ -1122,7 +1123,7 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
                     h->heavy_cols = dalloc<int32_t>(static_cast<size_t>(h->heavy_cap) * h->heavy_grid, st, "heavy staging");
                     h->heavy_vals = dalloc<double>(static_cast<size_t>(h->heavy_cap) * h->heavy_grid, st, "heavy staging");
                 }
-                cuda_check(launch_numeric_heavy(L, h->heavy_cols, h->heavy_vals, h->heavy_cap, kHeavyLogW, h->heavy_nb,
+                cuda_check(launch_numeric_heavy(L, h->heavy_cols, h->heavy_vals, h->heavy_cap, kHeavyBucketKeys, h->heavy_nb,
                                                 h->heavy_grid, st),
                            "numeric heavy kernel");
             } else if (pc.l2) {

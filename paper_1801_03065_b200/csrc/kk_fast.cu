@@ -524,37 +524,8 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                 bb = __ldg(b_rowptr + j);
                 bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
             }
-            FlatMap<false> fm;
-            fm.init(bb, bl, 0.0, lane, scratch);
-            const int32_t total = fm.total;
-            // window w0's (key, word) are loaded one window ahead
-            auto fetch = [&](int32_t w0, int32_t& key, uint32_t& word) {
-                const int32_t t = w0 + lane;
-                int32_t e;
-                int64_t base;
-                double a_unused;
-                fm.window(w0, lane, e, base, a_unused);
-                key = kEmpty;
-                word = 0u;
-                if (t < total) {
-                    const int64_t q = base + (t - e);
-                    if constexpr (kCompressed) {
-                        key = __ldg(L.csi + q);
-                        word = __ldg(L.cs + q);
-                    } else {
-                        key = __ldg(L.b_cols + q);
-                        word = 1u;
-                    }
-                }
-            };
-            int32_t nkey;
-            uint32_t nword;
-            fetch(0, nkey, nword);
-            for (int32_t w0 = 0; w0 < total; w0 += 32) {
-                const int32_t key = nkey;
-                const uint32_t word = nword;
-                if (w0 + 32 < total)
-                    fetch(w0 + 32, nkey, nword);
+            // probe / claim / OR one (key, word); true when this lane claimed a slot
+            auto insert = [&](int32_t key, uint32_t word) -> bool {
                 bool claimed = false;
                 if (key != kEmpty) {
                     uint32_t s = loc_hash(key, pshift);
@@ -576,12 +547,85 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                     if constexpr (kCompressed)
                         atomicOr(&words[s], word);
                 }
-                // claims are counted one window late (the ballot then never
-                // waits on this window's CAS); a table can fill up before the
-                // count sees it, but such a row is always flagged at its end
+                return claimed;
+            };
+            // claims are counted one step late (the ballot then never waits on
+            // this step's CAS); a table can fill up before the count sees it,
+            // but such a row is always flagged at its end
+            auto account = [&](bool claimed) {
                 used += __popc(__ballot_sync(kFull, prev_claimed));
                 prev_claimed = claimed;
-                if (used > cap) { // table too small for this row: hand it to the L2 path
+                return used > cap; // table too small for this row: hand it to the L2 path
+            };
+            auto load = [&](int64_t q, int32_t& key, uint32_t& word) {
+                if constexpr (kCompressed) {
+                    key = __ldg(L.csi + q);
+                    word = __ldg(L.cs + q);
+                } else {
+                    key = __ldg(L.b_cols + q);
+                    word = 1u;
+                }
+            };
+            const int32_t maxbl = static_cast<int32_t>(__reduce_max_sync(kFull, static_cast<unsigned>(bl)));
+            const int lg = maxbl <= 1 ? 0 : 32 - __clz(maxbl - 1);
+            const int G = 32 >> lg;
+            const int32_t csum = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<unsigned>(bl)));
+            if (!L.no_segments && maxbl <= 16 && (na + G - 1) / G <= (csum + 31) / 32) {
+                // short (compressed) B rows: segmented steps — G = 32/Lw B rows
+                // per step, Lw = pow2 >= the longest, lane = (row, entry); the
+                // union is order-free, so no flattened-index mapping is needed.
+                // Taken when it needs no more steps than 32-product windows.
+                const int sub = lane >> lg;
+                const int t = lane & ((1 << lg) - 1);
+                auto sfetch = [&](int q0, int32_t& key, uint32_t& word) {
+                    const int q = q0 + sub;
+                    const int qs = q < 32 ? q : 31;
+                    const int64_t b = __shfl_sync(kFull, bb, qs);
+                    const int32_t l = __shfl_sync(kFull, bl, qs);
+                    key = kEmpty;
+                    word = 0u;
+                    if (q < na && t < l)
+                        load(b + t, key, word);
+                };
+                int32_t nkey;
+                uint32_t nword;
+                sfetch(0, nkey, nword);
+                for (int q0 = 0; q0 < na; q0 += G) {
+                    const int32_t key = nkey;
+                    const uint32_t word = nword;
+                    if (q0 + G < na)
+                        sfetch(q0 + G, nkey, nword);
+                    if (account(insert(key, word))) {
+                        overflow = true;
+                        break;
+                    }
+                }
+                continue;
+            }
+            FlatMap<false> fm;
+            fm.init(bb, bl, 0.0, lane, scratch);
+            const int32_t total = fm.total;
+            // window w0's (key, word) are loaded one window ahead
+            auto fetch = [&](int32_t w0, int32_t& key, uint32_t& word) {
+                const int32_t t = w0 + lane;
+                int32_t e;
+                int64_t base;
+                double a_unused;
+                fm.window(w0, lane, e, base, a_unused);
+                key = kEmpty;
+                word = 0u;
+                if (t < total)
+                    load(base + (t - e), key, word);
+            };
+            int32_t nkey;
+            uint32_t nword;
+            fetch(0, nkey, nword);
+            for (int32_t w0 = 0; w0 < total; w0 += 32) {
+                const int32_t key = nkey;
+                const uint32_t word = nword;
+                if (w0 + 32 < total)
+                    fetch(w0 + 32, nkey, nword);
+                if (account(insert(key, word))) {
                     overflow = true;
                     break;
                 }
@@ -660,10 +704,12 @@ cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, unsigned l
         if (e != cudaSuccess)
             return e;
     }
+    RowLaunch Lx = L;
+    Lx.no_segments = getenv("KK_SYM_NOSEG") != nullptr;
     if (compressed)
-        symbolic_flat_kernel<true><<<L.grid, L.wpb * 32, smem, st>>>(L, retry_count, retry_list);
+        symbolic_flat_kernel<true><<<L.grid, L.wpb * 32, smem, st>>>(Lx, retry_count, retry_list);
     else
-        symbolic_flat_kernel<false><<<L.grid, L.wpb * 32, smem, st>>>(L, retry_count, retry_list);
+        symbolic_flat_kernel<false><<<L.grid, L.wpb * 32, smem, st>>>(Lx, retry_count, retry_list);
     count_launch();
     return cudaGetLastError();
 }

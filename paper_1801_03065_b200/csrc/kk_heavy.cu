@@ -5,17 +5,21 @@
 // symbolic_heavy_kernel: the structure union is order-independent, so the CTA
 //   ORs every (word index, word) of the row into a DENSE bitmap over the whole
 //   column domain in shared memory (the Dense accumulator, accumulators.hpp:
-//   279-349, with effective_k = ceil(k/32) words when compressed) and pops it.
+//   279-349, with effective_k = ceil(k/32) words when compressed) and pops the
+//   words it touched (a one-bit-per-word summary lists them).  Chunks with many
+//   products are split into windows over all 32 warps.
 //
 // numeric_heavy_kernel: values must be summed left to right per key
 //   (bit-exact vs the reference), so products are first scattered STABLY into
-//   column buckets of W columns (counting sort: per-warp-tile histograms,
-//   bucket-major scan, match-ranked scatter in product order), then each warp
-//   accumulates one bucket at a time into a dense shared-memory slab with the
-//   ordered in-window fold, and emits the bucket's columns in ascending order.
-//   Every product is read/written a bounded number of times (streaming), the
-//   only random accesses are to shared memory.  Heavy rows therefore come out
-//   column-sorted; their values are bitwise the reference's.
+//   hashed column buckets (~384 distinct columns each; counting sort: per-warp
+//   tile histograms, bucket-major scan, match-ranked scatter in product order),
+//   then each warp accumulates one bucket at a time into a 1024-slot shared
+//   hash table with the ordered in-window fold and emits it compacted.  Every
+//   product is read/written a bounded number of times (streaming); the only
+//   random accesses are to shared memory; per-row overhead is proportional to
+//   the row's output, not to the column domain.  Heavy rows therefore come out
+//   in bucket/slot order (the contract compares sorted rows); their values are
+//   bitwise the reference's.
 #include <cstdint>
 
 #include "kk_device.cuh"
@@ -139,27 +143,74 @@ template <bool kCompressed>
 __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L, int32_t words)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    // bm: dense bitmap of the column domain; sm: one bit per bm word, set on
+    // the word's first touch, so the count-and-clear pass visits touched words
+    // only (O(touched), not O(domain), per row)
     uint32_t* bm = reinterpret_cast<uint32_t*>(smem);
+    const int32_t swords = (words + 31) >> 5;
+    uint32_t* sm = bm + words;
     __shared__ unsigned long long red[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int t = threadIdx.x; t < words; t += blockDim.x)
+    for (int t = threadIdx.x; t < words + swords; t += blockDim.x)
         bm[t] = 0u;
     __syncthreads();
+    auto add = [&](int32_t w, uint32_t word) {
+        if (atomicOr(&bm[w], word) == 0u)
+            atomicOr(&sm[w >> 5], 1u << (w & 31));
+    };
     for (int64_t r = blockIdx.x; r < L.nrows; r += gridDim.x) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
         const int64_t abeg = __ldg(L.a_rowptr + i), aend = __ldg(L.a_rowptr + i + 1);
-        // warps take interleaved 32-entry chunks of A(i,:): the union is order-free
-        for (int64_t c = abeg + 32 * warp; c < aend; c += 32 * nw)
-            walk_products<false, kCompressed>(L, c, c + 32 < aend ? c + 32 : aend, lane,
-                                              [&](bool valid, int32_t key, uint32_t word, double) {
-                                                  if (valid)
-                                                      atomicOr(&bm[kCompressed ? key : (key >> 5)], word);
-                                              });
+        // chunks of 32 A entries: a chunk with many products is split into
+        // 32-product windows over all warps, a small one goes to one warp
+        // (the union is order-free)
+        for (int64_t c = abeg, ci = 0; c < aend; c += 32, ++ci) {
+            const int na = static_cast<int>(aend - c < 32 ? aend - c : 32);
+            int64_t bb = 0;
+            int32_t bl = 0;
+            if (lane < na) {
+                const int32_t j = __ldg(L.a_cols + c + lane);
+                bb = __ldg(L.b_rowptr + j);
+                bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(L.b_rowptr + j + 1) - bb);
+            }
+            const int32_t tot = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<unsigned>(bl)));
+            const bool split = tot >= 8 * 32;
+            if (!split && (ci % nw) != warp)
+                continue;
+            HMap fm;
+            fm.init(bb, bl, 0.0, lane);
+            const int32_t w_first = split ? 32 * warp : 0, w_step = split ? 32 * nw : 32;
+            for (int32_t w0 = w_first; w0 < tot; w0 += w_step) {
+                // segments that start before the window (windows are strided)
+                fm.rank = __popc(__ballot_sync(kFull, lane < fm.nne && fm.cexcl < w0));
+                int32_t e;
+                int64_t base;
+                double a_unused;
+                fm.window(w0, lane, e, base, a_unused);
+                const int32_t t = w0 + lane;
+                if (t < tot) {
+                    const int64_t q = base + (t - e);
+                    if constexpr (kCompressed) {
+                        add(__ldg(L.csi + q), __ldg(L.cs + q));
+                    } else {
+                        const int32_t key = __ldg(L.b_cols + q);
+                        add(key >> 5, 1u << (key & 31));
+                    }
+                }
+            }
+        }
         __syncthreads();
         unsigned long long cnt = 0;
-        for (int t = threadIdx.x; t < words; t += blockDim.x) {
-            cnt += __popc(bm[t]);
-            bm[t] = 0u;
+        for (int t = threadIdx.x; t < swords; t += blockDim.x) {
+            uint32_t sw = sm[t];
+            while (sw) {
+                const int b = __ffs(sw) - 1;
+                sw &= sw - 1;
+                const int32_t w = (t << 5) + b;
+                cnt += __popc(bm[w]);
+                bm[w] = 0u;
+            }
+            sm[t] = 0u;
         }
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1)
@@ -185,8 +236,8 @@ struct HeavyArgs {
     int32_t* stage_cols; // [num_ctas * stage_cap]
     double* stage_vals;
     int64_t stage_cap;   // products per CTA (>= max row flops)
-    int32_t logw;        // bucket width W = 1 << logw columns
-    int32_t nb;          // buckets (k / W rounded up)
+    int32_t bucket_keys; // target distinct columns per bucket
+    int32_t nb;          // maximum buckets per row
 };
 
 // block-wide exclusive scan of one int32 per thread (kHeavyThreads threads);
@@ -215,23 +266,37 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sh_warp, 
     return wpre + incl - v;
 }
 
+// per-warp bucket table (pass 3): linear probing, keys[kHeavyT] + vals[kHeavyT]
+constexpr int kHeavyT = 1024;
+constexpr int kHeavyTShift = 32 - 10;
+
+__device__ __forceinline__ int heavy_bucket(int32_t key, int nb)
+{
+    // multiply-shift range reduction of a Fibonacci hash: buckets balance the
+    // row's DISTINCT columns whatever their distribution (R-MAT hubs)
+    return static_cast<int>((static_cast<uint64_t>(static_cast<uint32_t>(key) * 0x9E3779B1u) * nb) >> 32);
+}
+
+__device__ __forceinline__ uint32_t heavy_slot(int32_t key)
+{
+    return (static_cast<uint32_t>(key) * 0x85EBCA6Bu) >> kHeavyTShift; // independent of the bucket hash
+}
+
 __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowLaunch L, const HeavyArgs H)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nb = H.nb;
-    const int W = 1 << H.logw;
-    // layout: bstart[nb+1] | bcount[nb] | outoff[nb] (int32) | union {
+    const int nb_max = H.nb;
+    // shared memory: bstart[nb+1] bcount[nb] outoff[nb] | union {
     //   off[kHeavyWarps][nb] int32            (passes 1-2: tile x bucket offsets)
-    //   per-warp dense slab vals[W] + bitmap  (pass 3) }
-    // The union keeps the CTA small enough for two CTAs per SM.
+    //   per-warp bucket tables keys[T] + vals[T] (pass 3) }
     int32_t* bstart = reinterpret_cast<int32_t*>(smem);
-    int32_t* bcount = bstart + nb + 1;
-    int32_t* outoff = bcount + nb;
-    const size_t head = ((size_t)(3 * nb + 1) * 4 + 15) / 16 * 16;
+    int32_t* bcount = bstart + nb_max + 1;
+    int32_t* outoff = bcount + nb_max;
+    const size_t head = ((size_t)(3 * nb_max + 1) * 4 + 15) / 16 * 16;
     int32_t* off = reinterpret_cast<int32_t*>(smem + head);
-    double* slab = reinterpret_cast<double*>(smem + head) + (size_t)warp * W;
-    uint32_t* bits = reinterpret_cast<uint32_t*>(smem + head + (size_t)kHeavyWarps * W * 8) + (size_t)warp * (W / 32);
+    double* tvals = reinterpret_cast<double*>(smem + head) + (size_t)warp * kHeavyT;
+    int32_t* tkeys = reinterpret_cast<int32_t*>(smem + head + (size_t)kHeavyWarps * kHeavyT * 8) + (size_t)warp * kHeavyT;
     __shared__ int32_t sh_warp[kHeavyWarps];
     __shared__ int64_t tile_lo[kHeavyWarps + 1];
     __shared__ int32_t next_bucket;
@@ -245,6 +310,9 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             continue; // outside the requested row range (spg_numeric_rows)
         const int64_t cbase = __ldg(L.c_rowptr + i);
         const int32_t cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
+        // buckets for this row: about H.bucket_keys distinct columns each
+        int nb = (cap + H.bucket_keys - 1) / H.bucket_keys;
+        nb = nb < 1 ? 1 : (nb > nb_max ? nb_max : nb);
         const int64_t abeg = __ldg(L.a_rowptr + i), aend = __ldg(L.a_rowptr + i + 1);
         const int64_t d = aend - abeg;
         // ---- product-balanced contiguous tiles of A entries, one per warp ----
@@ -290,7 +358,7 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
         const int64_t t_lo = tile_lo[warp], t_hi = tile_lo[warp + 1];
         // ---- pass 1: per-(tile, bucket) counts ----
         walk_products<true, false>(L, t_lo, t_hi, lane, [&](bool valid, int32_t key, uint32_t, double) {
-            const int b = valid ? (key >> H.logw) : -1;
+            const int b = valid ? heavy_bucket(key, nb) : -1;
             const uint32_t grp = __match_any_sync(kFull, b);
             if (b >= 0 && (__ffs(grp) - 1) == lane)
                 off[warp * nb + b] += __popc(grp);
@@ -298,33 +366,27 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
         __syncthreads();
         // ---- bucket-major exclusive scan -> stable offsets off[w][b] ----
         {
-            constexpr int kPer = 4; // buckets per thread (nb <= 1024)
-            int32_t tot[kPer];
+            const int per = (nb + kHeavyThreads - 1) / kHeavyThreads; // buckets per thread
+            const int b0 = threadIdx.x * per;
             int32_t mysum = 0;
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int b = threadIdx.x * kPer + u;
-                tot[u] = 0;
+            for (int u = 0; u < per; ++u) {
+                const int b = b0 + u;
                 if (b < nb)
                     for (int w = 0; w < kHeavyWarps; ++w)
-                        tot[u] += off[w * nb + b];
-                mysum += tot[u];
+                        mysum += off[w * nb + b];
             }
             int32_t all;
             int32_t run = block_excl_scan(mysum, sh_warp, &all);
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int b = threadIdx.x * kPer + u;
+            for (int u = 0; u < per; ++u) {
+                const int b = b0 + u;
                 if (b < nb) {
                     bstart[b] = run;
-                    int32_t rr = run;
                     for (int w = 0; w < kHeavyWarps; ++w) {
                         const int32_t c = off[w * nb + b];
-                        off[w * nb + b] = rr;
-                        rr += c;
+                        off[w * nb + b] = run;
+                        run += c;
                     }
                 }
-                run += tot[u];
             }
             if (threadIdx.x == 0)
                 bstart[nb] = all;
@@ -332,7 +394,7 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
         __syncthreads();
         // ---- pass 2: stable scatter of (col, a*b) into the CTA's staging ----
         walk_products<true, false>(L, t_lo, t_hi, lane, [&](bool valid, int32_t key, uint32_t, double v) {
-            const int b = valid ? (key >> H.logw) : -1;
+            const int b = valid ? heavy_bucket(key, nb) : -1;
             const uint32_t grp = __match_any_sync(kFull, b);
             const int leader = __ffs(grp) - 1;
             int32_t base = 0;
@@ -348,9 +410,10 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             }
         });
         __syncthreads();
-        // ---- pass 3: warps grab buckets dynamically; ordered dense accumulation ----
-        for (int t = lane; t < W / 32; t += 32) // the slab region aliased off[] in passes 1-2
-            bits[t] = 0u;
+        // ---- pass 3: warps grab buckets; ordered accumulation in a per-warp
+        //      hash table, emitted compacted at the bucket's start ----
+        for (int t = lane; t < kHeavyT; t += 32) // the tables aliased off[] in passes 1-2
+            tkeys[t] = kEmpty;
         __syncwarp();
         for (;;) {
             int b = 0;
@@ -360,17 +423,13 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             if (b >= nb)
                 break;
             const int32_t lo = bstart[b], hi = bstart[b + 1];
-            if (lo == hi) {
-                if (lane == 0)
-                    bcount[b] = 0;
-                continue;
-            }
             int32_t nkey = -1 - lane;
             double nv = 0.0;
             if (lo + lane < hi) {
-                nkey = scols[lo + lane] & (W - 1);
+                nkey = scols[lo + lane];
                 nv = svals[lo + lane];
             }
+            bool lost = false;
             for (int32_t w0 = lo; w0 < hi; w0 += 32) {
                 const int32_t q = w0 + lane;
                 const bool valid = q < hi;
@@ -380,18 +439,39 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
                 nkey = -1 - lane;
                 nv = 0.0;
                 if (q + 32 < hi) {
-                    nkey = scols[q + 32] & (W - 1);
+                    nkey = scols[q + 32];
                     nv = svals[q + 32];
                 }
                 const uint32_t grp = __match_any_sync(kFull, key);
                 const bool leader = valid && (__ffs(grp) - 1) == lane;
                 double acc = v;
+                uint32_t s = 0;
                 if (leader) {
-                    // leaders hold distinct keys but may share a bitmap word: atomic set
-                    const uint32_t m = 1u << (key & 31);
-                    if (atomicOr(&bits[key >> 5], m) & m)
-                        acc = __dadd_rn(slab[key], v);
-                    // else first touch: the running sum starts at this product
+                    // leaders hold distinct keys; a first touch claims a slot and
+                    // its running sum starts at this product
+                    s = heavy_slot(key);
+                    int probes = 0;
+                    for (;;) {
+                        const int32_t k = tkeys[s];
+                        if (k == key) {
+                            acc = __dadd_rn(tvals[s], v);
+                            break;
+                        }
+                        if (k == kEmpty) {
+                            const int32_t old = atomicCAS(&tkeys[s], kEmpty, key);
+                            if (old == kEmpty)
+                                break;
+                            if (old == key) {
+                                acc = __dadd_rn(tvals[s], v); // unreachable: leaders are distinct
+                                break;
+                            }
+                        }
+                        s = (s + 1) & (kHeavyT - 1);
+                        if (++probes >= kHeavyT) {
+                            lost = true;
+                            break;
+                        }
+                    }
                 }
                 uint32_t rest = leader ? (grp & (grp - 1)) : 0u;
                 const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(rest)));
@@ -404,34 +484,24 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
                     }
                 }
                 if (leader)
-                    slab[key] = acc;
+                    tvals[s] = acc;
                 __syncwarp();
             }
-            // emit the bucket's columns ascending, compacted in place at its start
+            if (__any_sync(kFull, lost) && lane == 0)
+                raise_error(L.ctr, kDevL2Overflow);
+            // emit the bucket's columns (table order), compacted in place at its start
             int32_t base = lo;
-            for (int t0 = 0; t0 < W / 32; t0 += 32) {
-                const uint32_t word = t0 + lane < W / 32 ? bits[t0 + lane] : 0u;
-                const int32_t c = __popc(word);
-                int32_t incl = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int32_t y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o)
-                        incl += y;
+            for (int t0 = 0; t0 < kHeavyT; t0 += 32) {
+                const int32_t k = tkeys[t0 + lane];
+                const bool hit = k != kEmpty;
+                const uint32_t m = __ballot_sync(kFull, hit);
+                if (hit) {
+                    const int32_t pos = base + __popc(m & lanemask_lt());
+                    scols[pos] = k;
+                    svals[pos] = tvals[t0 + lane];
+                    tkeys[t0 + lane] = kEmpty;
                 }
-                int32_t pos = base + incl - c;
-                uint32_t wb = word;
-                while (wb) {
-                    const int bit = __ffs(wb) - 1;
-                    wb &= wb - 1;
-                    const int32_t colw = ((t0 + lane) << 5) + bit;
-                    scols[pos] = (b << H.logw) + colw;
-                    svals[pos] = slab[colw];
-                    ++pos;
-                }
-                if (t0 + lane < W / 32)
-                    bits[t0 + lane] = 0u;
-                base += __shfl_sync(kFull, incl, 31);
+                base += __popc(m);
             }
             if (lane == 0)
                 bcount[b] = base - lo;
@@ -440,18 +510,15 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
         __syncthreads();
         // ---- output offsets of the buckets, then copy out ----
         {
-            constexpr int kPer = 4;
+            const int per = (nb + kHeavyThreads - 1) / kHeavyThreads;
+            const int b0 = threadIdx.x * per;
             int32_t mysum = 0;
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int b = threadIdx.x * kPer + u;
-                mysum += b < nb ? bcount[b] : 0;
-            }
+            for (int u = 0; u < per; ++u)
+                mysum += b0 + u < nb ? bcount[b0 + u] : 0;
             int32_t all;
             int32_t run = block_excl_scan(mysum, sh_warp, &all);
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const int b = threadIdx.x * kPer + u;
+            for (int u = 0; u < per; ++u) {
+                const int b = b0 + u;
                 if (b < nb) {
                     outoff[b] = run;
                     run += bcount[b];
@@ -478,20 +545,19 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
     }
 }
 
-// ---------------------------------------------------------------------------
-size_t heavy_numeric_smem(int nb, int logw)
+size_t heavy_numeric_smem(int nb, int /*bucket_keys*/)
 {
     const size_t head = ((size_t)(3 * nb + 1) * 4 + 15) / 16 * 16;
     const size_t hist = (size_t)kHeavyWarps * nb * 4;
-    const size_t slabs = (size_t)kHeavyWarps * ((size_t(1) << logw) * 8 + (size_t(1) << logw) / 8);
-    return head + (hist > slabs ? hist : slabs);
+    const size_t tables = (size_t)kHeavyWarps * kHeavyT * 12;
+    return head + (hist > tables ? hist : tables);
 }
 
 cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st)
 {
     if (L.nrows <= 0)
         return cudaSuccess;
-    const size_t smem = (size_t)words * 4;
+    const size_t smem = ((size_t)words + (words + 31) / 32) * 4;
     const void* fn = compressed ? reinterpret_cast<const void*>(&symbolic_heavy_kernel<true>)
                                 : reinterpret_cast<const void*>(&symbolic_heavy_kernel<false>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -506,16 +572,16 @@ cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t w
 }
 
 cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double* stage_vals, int64_t stage_cap,
-                                 int32_t logw, int32_t nb, int grid, cudaStream_t st)
+                                 int32_t bucket_keys, int32_t nb, int grid, cudaStream_t st)
 {
     if (L.nrows <= 0)
         return cudaSuccess;
-    const size_t smem = heavy_numeric_smem(nb, logw);
+    const size_t smem = heavy_numeric_smem(nb, bucket_keys);
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&numeric_heavy_kernel),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
-    HeavyArgs H{stage_cols, stage_vals, stage_cap, logw, nb};
+    HeavyArgs H{stage_cols, stage_vals, stage_cap, bucket_keys, nb};
     numeric_heavy_kernel<<<grid, kHeavyThreads, smem, st>>>(L, H);
     count_launch();
     return cudaGetLastError();

@@ -62,6 +62,7 @@ struct RowLaunch {
     int64_t nrows;
     int32_t row_lo, row_hi; // numeric: only rows in [row_lo, row_hi) when row_hi > 0
     const unsigned long long* gate; // numeric fast kernel: exit when gate[0..1] == gate[2..3] (replayed)
+    int32_t no_segments;            // symbolic fast kernel: always use 32-product windows (A/B switch)
     // outputs
     int64_t* sym_sizes;          // symbolic: sizes[i] (== rowptr + 1)
     const int64_t* c_rowptr;     // numeric
@@ -113,7 +114,7 @@ int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem);
 // heavy rows (kk_heavy.cu)
 cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st);
 cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double* stage_vals, int64_t stage_cap,
-                                 int32_t logw, int32_t nb, int grid, cudaStream_t st);
+                                 int32_t bucket_keys, int32_t nb, int grid, cudaStream_t st);
 
 // structure-reuse replay (kk_replay.cu)
 struct ReplayLaunch {

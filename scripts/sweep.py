@@ -14,7 +14,7 @@ a, wl = workload(cfg_id, scale)
 A = a.to_device()
 print(wl, flush=True)
 
-def timeit(fn, reps=3):
+def timeit(fn, reps=int(os.environ.get("SWEEP_REPS", "3"))):
     fn(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
