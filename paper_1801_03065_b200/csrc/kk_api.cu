@@ -111,9 +111,9 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kWarpSmemMax = 48 * 1024; // L1 accumulator budget per warp
 constexpr int32_t kHeavySymWords = 49152;     // 192 KB dense bitmap per CTA (heavy symbolic)
-constexpr int32_t kHeavyBucketKeys = 384;     // numeric heavy rows: ~distinct columns per hashed bucket
-constexpr int32_t kHeavyMaxBuckets = 1280;    // buckets per row (shared-memory histogram bound)
-constexpr int64_t kHeavyMaxRow = int64_t{kHeavyMaxBuckets} * 640; // <= 62.5% load of the 1024-slot tables
+constexpr int32_t kHeavyBucketKeys = 256;     // numeric heavy rows: ~distinct columns per hashed bucket
+constexpr int32_t kHeavyMaxBuckets = 1536;    // buckets per row (shared-memory histogram bound)
+constexpr int64_t kHeavyMaxRow = int64_t{kHeavyMaxBuckets} * 320; // <= 62.5% load of the 512-slot tables
 constexpr uint64_t kCtaSmem = 96 * 1024;     // two CTAs per SM
 
 // device-side allocation helper (stream ordered)
@@ -494,7 +494,7 @@ struct spg_handle {
     // heavy numeric rows (kk_heavy.cu): per-CTA staging for the bucket scatter
     bool num_heavy = false;
     int heavy_nb = 0;
-    int heavy_grid = 0;
+    int64_t heavy_stage = 0; // staging products
     int64_t heavy_cap = 0;
     int32_t* heavy_cols = nullptr;
     double* heavy_vals = nullptr;
@@ -598,6 +598,8 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
         cudaFreeAsync(h->d_num_list, st);
         h->d_num_list = nullptr;
     }
+    if (h->num_heavy)
+        h->num.need_list = true; // heavy rows are queued largest first
     if (h->num.need_list) {
         h->d_num_list = dalloc<int32_t>(std::max<int64_t>(h->info.m, 1), st, "numeric row list");
         auto* fill = dalloc<unsigned long long>(32, st, "fill");
@@ -606,6 +608,10 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
                                       h->d_num_list, st),
                    "numeric binning");
         cudaFreeAsync(fill, st);
+        if (h->num_heavy && h->d_prf) {
+            const PhaseClass& hc = h->num.classes[h->num.l2_class];
+            cuda_check(sort_rows_by_flops_desc(h->d_num_list + hc.off, hc.count, h->d_prf, st), "heavy row order");
+        }
     }
 }
 
@@ -1111,21 +1117,33 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
             L.grid = pc.grid;
             L.l2 = pc.l2;
             if (pc.l2 && h->num_heavy) {
+                const int64_t resident = int64_t{numeric_heavy_blocks_per_sm(h->heavy_nb)} * sm_count();
+                const int64_t want = std::max<int64_t>(1, std::min<int64_t>(resident, pc.count));
                 if (!h->heavy_cols) {
-                    // staging for the bucket scatter: one row's products per CTA,
-                    // as many CTAs as half the free memory allows (<= one per SM)
+                    // staging for the bucket scatter (12 B per product), shared by
+                    // the two size classes of heavy rows below: what every
+                    // resident CTA needs for the largest row, or half the free
+                    // memory, whichever is smaller (at least one largest row)
                     size_t free_b = 0, total_b = 0;
                     cudaMemGetInfo(&free_b, &total_b);
-                    const uint64_t per_cta = static_cast<uint64_t>(h->heavy_cap) * 12;
-                    const int64_t fit = static_cast<int64_t>((free_b / 2) / std::max<uint64_t>(per_cta, 1));
-                    // two CTAs per SM fit (hist and slabs share shared memory)
-                    h->heavy_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({fit, 2 * sm_count(), pc.count})));
-                    h->heavy_cols = dalloc<int32_t>(static_cast<size_t>(h->heavy_cap) * h->heavy_grid, st, "heavy staging");
-                    h->heavy_vals = dalloc<double>(static_cast<size_t>(h->heavy_cap) * h->heavy_grid, st, "heavy staging");
+                    const int64_t by_mem = static_cast<int64_t>(free_b / 2 / 12);
+                    h->heavy_stage = std::max<int64_t>(std::min<int64_t>(by_mem, h->heavy_cap * want), h->heavy_cap);
+                    h->heavy_cols = dalloc<int32_t>(static_cast<size_t>(h->heavy_stage), st, "heavy staging");
+                    h->heavy_vals = dalloc<double>(static_cast<size_t>(h->heavy_stage), st, "heavy staging");
                 }
-                cuda_check(launch_numeric_heavy(L, h->heavy_cols, h->heavy_vals, h->heavy_cap, kHeavyBucketKeys, h->heavy_nb,
-                                                h->heavy_grid, st),
+                // rows whose products fit an equal share of the staging run on
+                // every resident CTA; the largest rows then run with one
+                // largest-row stage per CTA
+                const int64_t small_cap = std::min<int64_t>(h->heavy_cap, h->heavy_stage / want);
+                cuda_check(launch_numeric_heavy(L, h->heavy_cols, h->heavy_vals, small_cap, kHeavyBucketKeys,
+                                                h->heavy_nb, -1, small_cap, 0, static_cast<int>(want), st),
                            "numeric heavy kernel");
+                if (small_cap < h->heavy_cap) {
+                    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(h->heavy_stage / h->heavy_cap, want));
+                    cuda_check(launch_numeric_heavy(L, h->heavy_cols, h->heavy_vals, h->heavy_cap, kHeavyBucketKeys,
+                                                    h->heavy_nb, small_cap, INT64_MAX, 1, static_cast<int>(g), st),
+                               "numeric heavy kernel (largest rows)");
+                }
             } else if (pc.l2) {
                 L.pool = PoolDesc{h->num_pool.base, P.l2.chunk_bytes, P.l2.num_chunks, P.l2.pool_mode,
                                   h->num_pool.states};

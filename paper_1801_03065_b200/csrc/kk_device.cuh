@@ -40,6 +40,7 @@ struct DevCounters {
     unsigned long long l2_inserts;
     int error;
     int pad;
+    unsigned long long next_row[2]; // heavy numeric launches: dynamic row queue heads
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()

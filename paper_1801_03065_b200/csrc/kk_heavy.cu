@@ -11,9 +11,9 @@
 //
 // numeric_heavy_kernel: values must be summed left to right per key
 //   (bit-exact vs the reference), so products are first scattered STABLY into
-//   hashed column buckets (~384 distinct columns each; counting sort: per-warp
+//   hashed column buckets (~256 distinct columns each; counting sort: per-warp
 //   tile histograms, bucket-major scan, match-ranked scatter in product order),
-//   then each warp accumulates one bucket at a time into a 1024-slot shared
+//   then each warp accumulates one bucket at a time into a 512-slot shared
 //   hash table with the ordered in-window fold and emits it compacted.  Every
 //   product is read/written a bounded number of times (streaming); the only
 //   random accesses are to shared memory; per-row overhead is proportional to
@@ -21,6 +21,8 @@
 //   in bucket/slot order (the contract compares sorted rows); their values are
 //   bitwise the reference's.
 #include <cstdint>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "kk_device.cuh"
 #include "kk_internal.h"
@@ -238,6 +240,8 @@ struct HeavyArgs {
     int64_t stage_cap;   // products per CTA (>= max row flops)
     int32_t bucket_keys; // target distinct columns per bucket
     int32_t nb;          // maximum buckets per row
+    int64_t min_products, max_products; // rows with products in (min, max] only
+    int32_t queue;                      // which DevCounters::next_row head this launch uses
 };
 
 // block-wide exclusive scan of one int32 per thread (kHeavyThreads threads);
@@ -267,8 +271,8 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sh_warp, 
 }
 
 // per-warp bucket table (pass 3): linear probing, keys[kHeavyT] + vals[kHeavyT]
-constexpr int kHeavyT = 1024;
-constexpr int kHeavyTShift = 32 - 10;
+constexpr int kHeavyT = 512;
+constexpr int kHeavyTShift = 32 - 9;
 
 __device__ __forceinline__ int heavy_bucket(int32_t key, int nb)
 {
@@ -301,10 +305,20 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
     __shared__ int64_t tile_lo[kHeavyWarps + 1];
     __shared__ int32_t next_bucket;
     __shared__ int32_t s_total;
+    __shared__ int64_t s_row;
     int32_t* scols = H.stage_cols + (size_t)blockIdx.x * H.stage_cap;
     double* svals = H.stage_vals + (size_t)blockIdx.x * H.stage_cap;
 
-    for (int64_t r = blockIdx.x; r < L.nrows; r += gridDim.x) {
+    // rows are taken from a queue (the list is ordered by decreasing products,
+    // so the largest rows start first and the tail is short)
+    for (;;) {
+        if (threadIdx.x == 0)
+            s_row = static_cast<int64_t>(atomicAdd(&L.ctr->next_row[H.queue], 1ull));
+        __syncthreads();
+        const int64_t r = s_row;
+        __syncthreads();
+        if (r >= L.nrows)
+            break;
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
         if (L.row_hi > 0 && (i < L.row_lo || i >= L.row_hi))
             continue; // outside the requested row range (spg_numeric_rows)
@@ -328,6 +342,8 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             tile_lo[threadIdx.x] = threadIdx.x == 0 ? abeg : aend;
         int32_t F;
         const int32_t before = block_excl_scan(mine, sh_warp, &F);
+        if (F <= H.min_products || F > H.max_products)
+            continue; // another launch (staging size class) takes this row
         if (threadIdx.x == 0) {
             s_total = F;
             next_bucket = 0;
@@ -553,6 +569,56 @@ size_t heavy_numeric_smem(int nb, int /*bucket_keys*/)
     return head + (hist > tables ? hist : tables);
 }
 
+__global__ void gather_row_flops_kernel(const int32_t* __restrict__ list, int64_t n, const int64_t* __restrict__ prf,
+                                        int64_t* __restrict__ keys)
+{
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        keys[t] = __ldg(prf + __ldg(list + t));
+}
+
+cudaError_t sort_rows_by_flops_desc(int32_t* list, int64_t n, const int64_t* prf, cudaStream_t st)
+{
+    if (n <= 1)
+        return cudaSuccess;
+    int64_t *k_in = nullptr, *k_out = nullptr;
+    int32_t* v_out = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp_bytes, k_in, k_out, list, v_out,
+                                                             static_cast<int>(n), 0, 64, st);
+    if (e == cudaSuccess)
+        e = cudaMallocAsync(&k_in, sizeof(int64_t) * n, st);
+    if (e == cudaSuccess)
+        e = cudaMallocAsync(&k_out, sizeof(int64_t) * n, st);
+    if (e == cudaSuccess)
+        e = cudaMallocAsync(&v_out, sizeof(int32_t) * n, st);
+    if (e == cudaSuccess)
+        e = cudaMallocAsync(&tmp, tmp_bytes, st);
+    if (e == cudaSuccess) {
+        gather_row_flops_kernel<<<sm_count() * 4, 256, 0, st>>>(list, n, prf, k_in);
+        count_launch();
+        e = cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, k_in, k_out, list, v_out, static_cast<int>(n),
+                                                     0, 64, st);
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(list, v_out, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st);
+    for (void* p : {static_cast<void*>(k_in), static_cast<void*>(k_out), static_cast<void*>(v_out), tmp})
+        if (p)
+            cudaFreeAsync(p, st);
+    return e;
+}
+
+int numeric_heavy_blocks_per_sm(int32_t nb)
+{
+    const size_t smem = heavy_numeric_smem(nb, 0);
+    const void* fn = reinterpret_cast<const void*>(&numeric_heavy_kernel);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kHeavyThreads, smem) != cudaSuccess)
+        return 1;
+    return b > 0 ? b : 1;
+}
+
 cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st)
 {
     if (L.nrows <= 0)
@@ -572,7 +638,8 @@ cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t w
 }
 
 cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double* stage_vals, int64_t stage_cap,
-                                 int32_t bucket_keys, int32_t nb, int grid, cudaStream_t st)
+                                 int32_t bucket_keys, int32_t nb, int64_t min_products, int64_t max_products,
+                                 int queue, int grid, cudaStream_t st)
 {
     if (L.nrows <= 0)
         return cudaSuccess;
@@ -581,7 +648,7 @@ cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
-    HeavyArgs H{stage_cols, stage_vals, stage_cap, bucket_keys, nb};
+    HeavyArgs H{stage_cols, stage_vals, stage_cap, bucket_keys, nb, min_products, max_products, queue};
     numeric_heavy_kernel<<<grid, kHeavyThreads, smem, st>>>(L, H);
     count_launch();
     return cudaGetLastError();

@@ -114,7 +114,10 @@ int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem);
 // heavy rows (kk_heavy.cu)
 cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st);
 cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double* stage_vals, int64_t stage_cap,
-                                 int32_t bucket_keys, int32_t nb, int grid, cudaStream_t st);
+                                 int32_t bucket_keys, int32_t nb, int64_t min_products, int64_t max_products,
+                                 int queue, int grid, cudaStream_t st);
+cudaError_t sort_rows_by_flops_desc(int32_t* list, int64_t n, const int64_t* prf, cudaStream_t st);
+int numeric_heavy_blocks_per_sm(int32_t nb);
 
 // structure-reuse replay (kk_replay.cu)
 struct ReplayLaunch {
