@@ -523,3 +523,38 @@ def test_numeric_rows_blocks_equal_full(kk, oracle, sort):
     assert h.replay_state == 2
     with pytest.raises(kk.ContractError):
         kk.numeric_rows(da, db, h, 10, 5, cols, vals)
+
+
+def test_short_and_long_rows_bitwise(kk, oracle):
+    """Rows of 0..40 A entries with 1..4-entry B rows (the flat kernel's
+    domain), empty rows and rows with more than 32 A entries mixed in the same
+    classes: raw order and value bits equal the reference's, also through
+    spg_numeric_rows and with compression on/off."""
+    import torch
+    rng = np.random.default_rng(57)
+    m, n, k = 3000, 2000, 5000
+    lens = rng.integers(0, 6, m)
+    lens[rng.choice(m, 40, replace=False)] = rng.integers(33, 41, 40)
+    lens[rng.choice(m, 200, replace=False)] = 0
+    rows = []
+    for i in range(m):
+        for c in rng.choice(n, lens[i], replace=False):
+            rows.append((i, int(c), float(rng.standard_normal())))
+    a = csr_from_triplets(m, n, rows)
+    brow = []
+    for i in range(n):
+        for c in rng.choice(k, int(rng.integers(1, 5)), replace=False):
+            brow.append((i, int(c), float(rng.standard_normal())))
+    b = csr_from_triplets(n, k, brow)
+    for mode in (kk.CompressionMode.Auto, kk.CompressionMode.Never, kk.CompressionMode.Always):
+        res = kk.multiply(a, b, kk.SpgemmConfig(compression=mode))
+        assert_parity(oracle, a, b, res.c.to_host())
+    da, db = a.to_device(), b.to_device()
+    h = kk.symbolic(da, db)
+    full = kk.numeric(da, db, h).to_host()
+    cols = torch.full((h.nnz_c(),), -3, dtype=torch.int32, device="cuda")
+    vals = torch.zeros(h.nnz_c(), dtype=torch.float64, device="cuda")
+    for r0, r1 in ((0, 1000), (1000, 1001), (1001, 2999), (2999, 3000)):
+        kk.numeric_rows(da, db, h, r0, r1, cols, vals)
+    assert np.array_equal(cols.cpu().numpy(), full.col_indices)
+    assert np.array_equal(vals.cpu().numpy().view(np.int64), full.values.view(np.int64))
