@@ -496,8 +496,7 @@ struct spg_handle {
     int heavy_nb = 0;
     int64_t heavy_stage = 0; // staging products
     int64_t heavy_cap = 0;
-    int32_t* heavy_cols = nullptr;
-    double* heavy_vals = nullptr;
+    void* heavy_stage_buf = nullptr; // 16-byte {column, value} records
     // structure-reuse replay (kk_replay.cu): recorded on the second numeric
     // pass, replayed from the third while the structure fingerprints match
     int numeric_calls = 0;
@@ -531,10 +530,8 @@ struct spg_handle {
     ~spg_handle()
     {
         free_replay();
-        if (heavy_cols)
-            cudaFree(heavy_cols);
-        if (heavy_vals)
-            cudaFree(heavy_vals);
+        if (heavy_stage_buf)
+            cudaFree(heavy_stage_buf);
         if (d_rowptr)
             cudaFree(d_rowptr);
         if (d_prf)
@@ -1119,28 +1116,27 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
             if (pc.l2 && h->num_heavy) {
                 const int64_t resident = int64_t{numeric_heavy_blocks_per_sm(h->heavy_nb)} * sm_count();
                 const int64_t want = std::max<int64_t>(1, std::min<int64_t>(resident, pc.count));
-                if (!h->heavy_cols) {
-                    // staging for the bucket scatter (12 B per product), shared by
+                if (!h->heavy_stage_buf) {
+                    // staging for the bucket scatter (16 B per product), shared by
                     // the two size classes of heavy rows below: what every
                     // resident CTA needs for the largest row, or half the free
                     // memory, whichever is smaller (at least one largest row)
                     size_t free_b = 0, total_b = 0;
                     cudaMemGetInfo(&free_b, &total_b);
-                    const int64_t by_mem = static_cast<int64_t>(free_b / 2 / 12);
+                    const int64_t by_mem = static_cast<int64_t>(free_b / 2 / 16);
                     h->heavy_stage = std::max<int64_t>(std::min<int64_t>(by_mem, h->heavy_cap * want), h->heavy_cap);
-                    h->heavy_cols = dalloc<int32_t>(static_cast<size_t>(h->heavy_stage), st, "heavy staging");
-                    h->heavy_vals = dalloc<double>(static_cast<size_t>(h->heavy_stage), st, "heavy staging");
+                    h->heavy_stage_buf = dalloc<double>(2 * static_cast<size_t>(h->heavy_stage), st, "heavy staging");
                 }
                 // rows whose products fit an equal share of the staging run on
                 // every resident CTA; the largest rows then run with one
                 // largest-row stage per CTA
                 const int64_t small_cap = std::min<int64_t>(h->heavy_cap, h->heavy_stage / want);
-                cuda_check(launch_numeric_heavy(L, h->heavy_cols, h->heavy_vals, small_cap, kHeavyBucketKeys,
+                cuda_check(launch_numeric_heavy(L, h->heavy_stage_buf, small_cap, kHeavyBucketKeys,
                                                 h->heavy_nb, -1, small_cap, 0, static_cast<int>(want), st),
                            "numeric heavy kernel");
                 if (small_cap < h->heavy_cap) {
                     const int64_t g = std::max<int64_t>(1, std::min<int64_t>(h->heavy_stage / h->heavy_cap, want));
-                    cuda_check(launch_numeric_heavy(L, h->heavy_cols, h->heavy_vals, h->heavy_cap, kHeavyBucketKeys,
+                    cuda_check(launch_numeric_heavy(L, h->heavy_stage_buf, h->heavy_cap, kHeavyBucketKeys,
                                                     h->heavy_nb, small_cap, INT64_MAX, 1, static_cast<int>(g), st),
                                "numeric heavy kernel (largest rows)");
                 }

@@ -235,8 +235,7 @@ __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L,
 // numeric: stable column-bucket scatter + ordered dense accumulation
 // ---------------------------------------------------------------------------
 struct HeavyArgs {
-    int32_t* stage_cols; // [num_ctas * stage_cap]
-    double* stage_vals;
+    longlong2* stage;    // [num_ctas * stage_cap] records {column, value bits}: one 16-byte store per product
     int64_t stage_cap;   // products per CTA (>= max row flops)
     int32_t bucket_keys; // target distinct columns per bucket
     int32_t nb;          // maximum buckets per row
@@ -306,8 +305,7 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
     __shared__ int32_t next_bucket;
     __shared__ int32_t s_total;
     __shared__ int64_t s_row;
-    int32_t* scols = H.stage_cols + (size_t)blockIdx.x * H.stage_cap;
-    double* svals = H.stage_vals + (size_t)blockIdx.x * H.stage_cap;
+    longlong2* srec = H.stage + (size_t)blockIdx.x * H.stage_cap;
 
     // rows are taken from a queue (the list is ordered by decreasing products,
     // so the largest rows start first and the tail is short)
@@ -421,8 +419,7 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             base = __shfl_sync(kFull, base, leader);
             if (b >= 0) {
                 const int32_t pos = base + __popc(grp & lanemask_lt());
-                scols[pos] = key;
-                svals[pos] = v;
+                srec[pos] = make_longlong2(key, __double_as_longlong(v));
             }
         });
         __syncthreads();
@@ -442,8 +439,9 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             int32_t nkey = -1 - lane;
             double nv = 0.0;
             if (lo + lane < hi) {
-                nkey = scols[lo + lane];
-                nv = svals[lo + lane];
+                const longlong2 rc = srec[lo + lane];
+                nkey = static_cast<int32_t>(rc.x);
+                nv = __longlong_as_double(rc.y);
             }
             bool lost = false;
             for (int32_t w0 = lo; w0 < hi; w0 += 32) {
@@ -455,8 +453,9 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
                 nkey = -1 - lane;
                 nv = 0.0;
                 if (q + 32 < hi) {
-                    nkey = scols[q + 32];
-                    nv = svals[q + 32];
+                    const longlong2 rc = srec[q + 32];
+                    nkey = static_cast<int32_t>(rc.x);
+                    nv = __longlong_as_double(rc.y);
                 }
                 const uint32_t grp = __match_any_sync(kFull, key);
                 const bool leader = valid && (__ffs(grp) - 1) == lane;
@@ -513,8 +512,7 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
                 const uint32_t m = __ballot_sync(kFull, hit);
                 if (hit) {
                     const int32_t pos = base + __popc(m & lanemask_lt());
-                    scols[pos] = k;
-                    svals[pos] = tvals[t0 + lane];
+                    srec[pos] = make_longlong2(k, __double_as_longlong(tvals[t0 + lane]));
                     tkeys[t0 + lane] = kEmpty;
                 }
                 base += __popc(m);
@@ -548,8 +546,9 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
             const int32_t lo = bstart[b], c = bcount[b], o = outoff[b];
             for (int32_t q = lane; q < c; q += 32) {
                 if (o + q < cap) {
-                    L.c_cols[cbase + o + q] = scols[lo + q];
-                    L.c_vals[cbase + o + q] = svals[lo + q];
+                    const longlong2 rc = srec[lo + q];
+                    L.c_cols[cbase + o + q] = static_cast<int32_t>(rc.x);
+                    L.c_vals[cbase + o + q] = __longlong_as_double(rc.y);
                 }
             }
         }
@@ -637,7 +636,7 @@ cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t w
     return cudaGetLastError();
 }
 
-cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double* stage_vals, int64_t stage_cap,
+cudaError_t launch_numeric_heavy(const RowLaunch& L, void* stage, int64_t stage_cap,
                                  int32_t bucket_keys, int32_t nb, int64_t min_products, int64_t max_products,
                                  int queue, int grid, cudaStream_t st)
 {
@@ -648,7 +647,7 @@ cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
-    HeavyArgs H{stage_cols, stage_vals, stage_cap, bucket_keys, nb, min_products, max_products, queue};
+    HeavyArgs H{static_cast<longlong2*>(stage), stage_cap, bucket_keys, nb, min_products, max_products, queue};
     numeric_heavy_kernel<<<grid, kHeavyThreads, smem, st>>>(L, H);
     count_launch();
     return cudaGetLastError();

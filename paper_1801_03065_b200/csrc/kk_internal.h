@@ -113,7 +113,7 @@ int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem);
 
 // heavy rows (kk_heavy.cu)
 cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st);
-cudaError_t launch_numeric_heavy(const RowLaunch& L, int32_t* stage_cols, double* stage_vals, int64_t stage_cap,
+cudaError_t launch_numeric_heavy(const RowLaunch& L, void* stage, int64_t stage_cap,
                                  int32_t bucket_keys, int32_t nb, int64_t min_products, int64_t max_products,
                                  int queue, int grid, cudaStream_t st);
 cudaError_t sort_rows_by_flops_desc(int32_t* list, int64_t n, const int64_t* prf, cudaStream_t st);
