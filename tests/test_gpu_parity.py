@@ -558,3 +558,36 @@ def test_short_and_long_rows_bitwise(kk, oracle):
         kk.numeric_rows(da, db, h, r0, r1, cols, vals)
     assert np.array_equal(cols.cpu().numpy(), full.col_indices)
     assert np.array_equal(vals.cpu().numpy().view(np.int64), full.values.view(np.int64))
+
+
+def test_numeric_reuse_is_graph_capturable(kk, oracle):
+    """Once a handle replays (third numeric pass on), spg_numeric is fully
+    stream-ordered: the reuse loop can be captured in a CUDA graph and replayed
+    with new values written into the same device buffers."""
+    import torch
+    rng = np.random.default_rng(61)
+    a = random_csr(rng, 400, 400, 0.06)
+    b = random_csr(rng, 400, 400, 0.06)
+    da, db = a.to_device(), b.to_device()
+    h = kk.symbolic(da, db)
+    nnz = h.nnz_c()
+    cols = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        kk.numeric(da, db, h, out=(cols, vals))
+    assert h.replay_state == 2
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        kk.numeric(da, db, h, stream=s, out=(cols, vals))  # warm the allocator on this stream
+        with torch.cuda.graph(g, stream=s):
+            kk.numeric(da, db, h, stream=s, out=(cols, vals))
+    torch.cuda.current_stream().wait_stream(s)
+    for f in (1.0, -2.5, 0.125):
+        da.values.copy_(torch.from_numpy(a.values * f))
+        g.replay()
+        torch.cuda.synchronize()
+        ap = kk.CsrMatrix(a.num_rows, a.num_cols, a.row_offsets, a.col_indices, a.values * f, a.sorted_rows)
+        c = kk.CsrMatrix(a.num_rows, b.num_cols, h.c_row_offsets, cols.cpu().numpy(), vals.cpu().numpy())
+        assert_parity(oracle, ap, b, c)
