@@ -844,7 +844,8 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         Totals* d_tot = dalloc<Totals>(1, st, "totals");
         ScanTotals* d_stot = dalloc<ScanTotals>(1, st, "scan totals");
 
-        PinnedBuf pin(sizeof(Totals) + sizeof(ScanTotals) + sizeof(DevCounters) + 64);
+        int* d_crange = dalloc<int>(2, st, "column range");
+        PinnedBuf pin(sizeof(Totals) + sizeof(ScanTotals) + sizeof(DevCounters) + 64 + 16);
         auto* htot = static_cast<Totals*>(pin.p);
         auto* hstot = reinterpret_cast<ScanTotals*>(htot + 1);
         auto* hctr = reinterpret_cast<DevCounters*>(hstot + 1);
@@ -854,6 +855,10 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         cuda_check(cudaMemcpyAsync(hviews + 1, a->row_offsets + m, 8, cudaMemcpyDeviceToHost, st), "A view");
         cuda_check(cudaMemcpyAsync(hviews + 2, b->row_offsets, 8, cudaMemcpyDeviceToHost, st), "B view");
         cuda_check(cudaMemcpyAsync(hviews + 3, b->row_offsets + n, 8, cudaMemcpyDeviceToHost, st), "B view");
+        // the band of B rows A references (only those are compressed)
+        int* hcrange = reinterpret_cast<int*>(hviews + 8);
+        cuda_check(launch_col_range(m, a->row_offsets, a->col_indices, d_crange, st), "column range");
+        cuda_check(cudaMemcpyAsync(hcrange, d_crange, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "column range");
         cuda_check(cudaEventRecord(ev[0], st), "event");
         cuda_check(cudaMemsetAsync(d_tot, 0, sizeof(Totals), st), "memset");
         cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");
@@ -869,7 +874,10 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         uint32_t* d_cs = d_cs_alloc - bview[0];
 
         // ---- K3 + K1/K4 ----
-        cuda_check(launch_compress(n, b->row_offsets, b->col_indices, d_csize, d_csi, d_cs, st), "compress");
+        const int32_t j0 = std::clamp(hcrange[0], 0, n), j1 = std::clamp(hcrange[1] + 1, j0, n);
+        cudaFreeAsync(d_crange, st);
+        cuda_check(launch_compress(j1 - j0, b->row_offsets + j0, b->col_indices, d_csize + j0, d_csi, d_cs, st),
+                   "compress");
         const double avg_len = m > 0 ? static_cast<double>(a->nnz) / m : 0.0;
         cuda_check(launch_flops(m, avg_len, a->row_offsets, a->col_indices, b->row_offsets, d_csize,
                                 h->d_prf, d_prcf, d_tot, st),

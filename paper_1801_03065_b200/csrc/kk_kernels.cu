@@ -710,6 +710,38 @@ cudaError_t scan_sizes_inplace(int64_t* rowptr, int64_t m, ScanTotals* tot, cuda
     return inclusive_scan(rowptr + 1, m, tot, st);
 }
 
+// [min, max] column index of A's entries: the B rows A can reference.  A row
+// block of a banded matrix (a multi-GPU shard) references a band of B, and
+// only that band is compressed.
+__global__ void __launch_bounds__(256) col_range_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,
+                                                        const int32_t* __restrict__ a_cols, int* out2)
+{
+    const int64_t lo = __ldg(a_rowptr), hi = __ldg(a_rowptr + m);
+    int mn = INT_MAX, mx = INT_MIN;
+    for (int64_t q = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += (int64_t)gridDim.x * blockDim.x) {
+        const int c = __ldg(a_cols + q);
+        mn = c < mn ? c : mn;
+        mx = c > mx ? c : mx;
+    }
+    mn = __reduce_min_sync(kFull, mn);
+    mx = __reduce_max_sync(kFull, mx);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out2, mn);
+        atomicMax(out2 + 1, mx);
+    }
+}
+
+cudaError_t launch_col_range(int32_t m, const int64_t* a_rowptr, const int32_t* a_cols, int* out2, cudaStream_t st)
+{
+    const int init[2] = {INT_MAX, INT_MIN};
+    cudaError_t e = cudaMemcpyAsync(out2, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess || m <= 0)
+        return e;
+    col_range_kernel<<<sm_count() * 4, 256, 0, st>>>(m, a_rowptr, a_cols, out2);
+    count_launch();
+    return cudaGetLastError();
+}
+
 // per-row flops only (K1 without compression): the flop-balanced row
 // partition of the multi-GPU path.  Warp per row.
 __global__ void __launch_bounds__(256) row_flops_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,
