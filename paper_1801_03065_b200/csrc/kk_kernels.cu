@@ -88,17 +88,14 @@ constexpr int32_t kShortRow = 8;
 // Thread per B row for rows of <= kShortRow entries:
 // the running (csi, cs) pair stays in registers and is flushed when the word
 // changes; an out-of-order word (unsorted row) merges into its earlier pair.
-// Longer rows are appended to `long_list` for the warp kernel below.
+// Longer rows are left to the warp kernel below.
 __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                              const int32_t* __restrict__ cols,
                                                              int32_t* __restrict__ csize,
                                                              int32_t* __restrict__ csi,
-                                                             uint32_t* __restrict__ cs,
-                                                             unsigned int* long_count,
-                                                             int32_t* __restrict__ long_list)
+                                                             uint32_t* __restrict__ cs)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int lane = threadIdx.x & 31;
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += stride) { // warp-uniform trips
         const int64_t j = b0 + threadIdx.x;
         int64_t lo = 0;
@@ -107,17 +104,8 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const in
             lo = __ldg(rowptr + j);
             len = static_cast<int32_t>(__ldg(rowptr + j + 1) - lo);
         }
-        // rows beyond kShortRow go to the warp kernel (warp-aggregated append)
+        // rows beyond kShortRow are the warp kernel's
         const bool is_long = j < n && len > kShortRow;
-        const uint32_t lm = __ballot_sync(kFull, is_long);
-        if (lm) {
-            unsigned int base = 0;
-            if (lane == __ffs(lm) - 1)
-                base = atomicAdd(long_count, static_cast<unsigned int>(__popc(lm)));
-            base = __shfl_sync(kFull, base, __ffs(lm) - 1);
-            if (is_long)
-                long_list[base + __popc(lm & lanemask_lt())] = static_cast<int32_t>(j);
-        }
         if (j >= n || is_long)
             continue;
         int32_t np = 0, cur_w = -1, maxw = -1;
@@ -157,39 +145,91 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const in
     }
 }
 
+__device__ __forceinline__ void compress_row_short(int64_t j, int64_t lo, int64_t len, int32_t col, int lane,
+                                                   int32_t* __restrict__ csize, int32_t* __restrict__ csi,
+                                                   uint32_t* __restrict__ cs)
+{
+    const bool valid = lane < len;
+    const int32_t w = col >> 5;
+    const int32_t key = valid ? w : -1 - lane;
+    const uint32_t grp = __match_any_sync(kFull, key);
+    const uint32_t orv = group_or(grp, valid ? (1u << (col & 31)) : 0u, lane);
+    const bool leader = valid && (__ffs(grp) - 1) == lane;
+    const uint32_t lm = __ballot_sync(kFull, leader);
+    if (leader) {
+        const int pos = __popc(lm & lanemask_lt());
+        csi[lo + pos] = w;
+        cs[lo + pos] = orv;
+    }
+    if (lane == 0)
+        csize[j] = __popc(lm);
+}
+
+__device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
+                                  int32_t* __restrict__ csize, int32_t* __restrict__ csi, uint32_t* __restrict__ cs);
+
+// Warp kernel for rows of more than kShortRow entries.  A warp takes batches
+// of 32 consecutive rows: one coalesced load of their offsets, then the long
+// rows of the batch (ballot) one after another, the next row's columns
+// loaded while the current one is compressed.
 __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ cols,
                                                        int32_t* __restrict__ csize,
                                                        int32_t* __restrict__ csi,
-                                                       uint32_t* __restrict__ cs,
-                                                       const unsigned int* list_count,
-                                                       const int32_t* __restrict__ list)
+                                                       uint32_t* __restrict__ cs)
 {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    const int64_t nrows = list ? static_cast<int64_t>(*list_count) : n;
-    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nrows; r += warps) {
-        const int64_t j = list ? list[r] : r;
-        const int64_t lo = __ldg(rowptr + j);
-        const int64_t len = __ldg(rowptr + j + 1) - lo;
-        if (len <= 32) {
-            const bool valid = lane < len;
-            const int32_t col = valid ? __ldg(cols + lo + lane) : 0;
-            const int32_t w = col >> 5;
-            const int32_t key = valid ? w : -1 - lane;
-            const uint32_t grp = __match_any_sync(kFull, key);
-            const uint32_t orv = group_or(grp, valid ? (1u << (col & 31)) : 0u, lane);
-            const bool leader = valid && (__ffs(grp) - 1) == lane;
-            const uint32_t lm = __ballot_sync(kFull, leader);
-            if (leader) {
-                const int pos = __popc(lm & lanemask_lt());
-                csi[lo + pos] = w;
-                cs[lo + pos] = orv;
-            }
-            if (lane == 0)
-                csize[j] = __popc(lm);
-            continue;
+    for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < n; r0 += warps * 32) {
+        const int64_t jr = r0 + lane;
+        int64_t blo = 0, blen = 0;
+        if (jr < n) {
+            blo = __ldg(rowptr + jr);
+            blen = __ldg(rowptr + jr + 1) - blo;
         }
+        uint32_t todo = __ballot_sync(kFull, jr < n && blen > kShortRow);
+        auto pop = [&]() {
+            const int q = todo ? __ffs(todo) - 1 : -1;
+            todo &= todo - 1;
+            return q;
+        };
+        auto fetch = [&](int q, int64_t& lo, int64_t& len, int32_t& col) {
+            lo = __shfl_sync(kFull, blo, q);
+            len = __shfl_sync(kFull, blen, q);
+            col = 0;
+            if (len <= 32 && lane < len)
+                col = __ldg(cols + lo + lane);
+        };
+        auto process = [&](int q, int64_t lo, int64_t len, int32_t col) {
+            if (len <= 32)
+                compress_row_short(r0 + q, lo, len, col, lane, csize, csi, cs);
+            else
+                compress_row_long(r0 + q, lo, len, cols, lane, csize, csi, cs);
+        };
+        int64_t loA = 0, lenA = 0, loB = 0, lenB = 0;
+        int32_t colA = 0, colB = 0;
+        int qa = pop();
+        if (qa >= 0)
+            fetch(qa, loA, lenA, colA);
+        while (qa >= 0) { // two register sets: a prefetched load is never copied
+            const int qb = pop();
+            if (qb >= 0)
+                fetch(qb, loB, lenB, colB);
+            process(qa, loA, lenA, colA);
+            if (qb < 0)
+                break;
+            qa = pop();
+            if (qa >= 0)
+                fetch(qa, loA, lenA, colA);
+            process(qb, loB, lenB, colB);
+        }
+    }
+}
+
+__device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
+                                  int32_t* __restrict__ csize, int32_t* __restrict__ csi, uint32_t* __restrict__ cs)
+{
+    {
         // long row: sortedness first (one extra read of the row, L1/L2 resident)
         bool sorted = true;
         int32_t prev_last = INT_MIN;
@@ -908,21 +948,13 @@ cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b
 {
     if (n <= 0)
         return cudaSuccess;
-    // short rows: thread per row; long rows (> 32): warp per row from a list
-    // whose length stays on the device (no host sync)
-    unsigned int* cnt = nullptr;
-    int32_t* list = nullptr;
-    cudaError_t e = cudaMallocAsync(&cnt, sizeof(unsigned int) + sizeof(int32_t) * (size_t)n, st);
-    if (e != cudaSuccess)
-        return e;
-    list = reinterpret_cast<int32_t*>(cnt + 1);
-    cudaMemsetAsync(cnt, 0, sizeof(unsigned int), st);
+    // short rows: thread per row; longer rows: warp per row in batches of 32
     const int tblocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
-    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs, cnt, list);
-    const int blocks = sm_count() * 4;
-    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs, cnt, list);
+    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs);
     count_launch();
-    cudaFreeAsync(cnt, st);
+    const int64_t batches = (n + 31) / 32;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((batches + 7) / 8, (int64_t)sm_count() * 8));
+    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs);
     count_launch();
     return cudaGetLastError();
 }
