@@ -839,8 +839,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         int32_t* d_csize = dalloc<int32_t>(std::max(n, 1), st, "csize");
         // B slots hold the compressed pairs; index them like B (base-relative)
         int64_t bview[2] = {0, 0}, aview[2] = {0, 0};
-        int32_t* d_csi_alloc = dalloc<int32_t>(std::max<int64_t>(b->nnz, 1), st, "csi");
-        uint32_t* d_cs_alloc = dalloc<uint32_t>(std::max<int64_t>(b->nnz, 1), st, "cs");
+        int2* d_cp_alloc = dalloc<int2>(std::max<int64_t>(b->nnz, 1), st, "compressed pairs");
         Totals* d_tot = dalloc<Totals>(1, st, "totals");
         ScanTotals* d_stot = dalloc<ScanTotals>(1, st, "scan totals");
 
@@ -870,13 +869,12 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         bview[1] = hviews[3];
         if (row_offsets_base_and_end(a, aview) != a->nnz || row_offsets_base_and_end(b, bview) != b->nnz)
             fail(SPG_ERR_CONTRACT, "symbolic: nnz does not match row_offsets");
-        int32_t* d_csi = d_csi_alloc - bview[0];
-        uint32_t* d_cs = d_cs_alloc - bview[0];
+        int2* d_cp = d_cp_alloc - bview[0];
 
         // ---- K3 + K1/K4 ----
         const int32_t j0 = std::clamp(hcrange[0], 0, n), j1 = std::clamp(hcrange[1] + 1, j0, n);
         cudaFreeAsync(d_crange, st);
-        cuda_check(launch_compress(j1 - j0, b->row_offsets + j0, b->col_indices, d_csize + j0, d_csi, d_cs, st),
+        cuda_check(launch_compress(j1 - j0, b->row_offsets + j0, b->col_indices, d_csize + j0, d_cp, st),
                    "compress");
         const double avg_len = m > 0 ? static_cast<double>(a->nnz) / m : 0.0;
         cuda_check(launch_flops(m, avg_len, a->row_offsets, a->col_indices, b->row_offsets, d_csize,
@@ -959,8 +957,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             L.b_rowptr = b->row_offsets;
             L.b_cols = b->col_indices;
             L.csize = d_csize;
-            L.csi = d_csi;
-            L.cs = d_cs;
+            L.cpair = d_cp;
             L.list = list;
             L.nrows = nrows;
             L.sym_sizes = h->d_rowptr + 1;
@@ -1015,8 +1012,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             cudaFreeAsync(d_list, st);
         cudaFreeAsync(d_prcf, st);
         cudaFreeAsync(d_csize, st);
-        cudaFreeAsync(d_csi_alloc, st);
-        cudaFreeAsync(d_cs_alloc, st);
+        cudaFreeAsync(d_cp_alloc, st);
         cudaFreeAsync(d_tot, st);
         cudaFreeAsync(d_stot, st);
         if (spool.base) {

@@ -100,12 +100,14 @@ struct CompressedSource {
     using Payload = uint32_t;
     const int64_t* __restrict__ rowptr;
     const int32_t* __restrict__ csize;
-    const int32_t* __restrict__ csi;
-    const uint32_t* __restrict__ cs;
+    const int2* __restrict__ cp; // {word index, bits}
     __device__ __forceinline__ int64_t base(int32_t j) const { return __ldg(rowptr + j); }
     __device__ __forceinline__ int64_t len(int32_t j) const { return __ldg(csize + j); }
-    __device__ __forceinline__ int32_t key(int64_t q) const { return __ldg(csi + q); }
-    __device__ __forceinline__ uint32_t payload(int64_t q, double) const { return __ldg(cs + q); }
+    __device__ __forceinline__ int32_t key(int64_t q) const { return __ldg(&cp[q].x); }
+    __device__ __forceinline__ uint32_t payload(int64_t q, double) const
+    {
+        return static_cast<uint32_t>(__ldg(&cp[q].y));
+    }
 };
 
 // ---- key -> first-touch position maps ------------------------------------------

@@ -559,8 +559,9 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
             };
             auto load = [&](int64_t q, int32_t& key, uint32_t& word) {
                 if constexpr (kCompressed) {
-                    key = __ldg(L.csi + q);
-                    word = __ldg(L.cs + q);
+                    const int2 pr = __ldg(L.cpair + q);
+                    key = pr.x;
+                    word = static_cast<uint32_t>(pr.y);
                 } else {
                     key = __ldg(L.b_cols + q);
                     word = 1u;

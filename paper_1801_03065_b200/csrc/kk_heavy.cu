@@ -108,8 +108,9 @@ __device__ __forceinline__ void walk_products(const RowLaunch& L, int64_t p_lo, 
             if (t < fm.total) {
                 const int64_t q = base + (t - e);
                 if constexpr (kCompressed) {
-                    key = __ldg(L.csi + q);
-                    word = __ldg(L.cs + q);
+                    const int2 pr = __ldg(L.cpair + q);
+                    key = pr.x;
+                    word = static_cast<uint32_t>(pr.y);
                 } else {
                     key = __ldg(L.b_cols + q); // raw column: its word bit is set at use
                     if constexpr (kNumeric)
@@ -193,7 +194,8 @@ __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L,
                 if (t < tot) {
                     const int64_t q = base + (t - e);
                     if constexpr (kCompressed) {
-                        add(__ldg(L.csi + q), __ldg(L.cs + q));
+                        const int2 pr = __ldg(L.cpair + q);
+                        add(pr.x, static_cast<uint32_t>(pr.y));
                     } else {
                         const int32_t key = __ldg(L.b_cols + q);
                         add(key >> 5, 1u << (key & 31));

@@ -55,8 +55,7 @@ struct RowLaunch {
     const int32_t* b_cols;
     const double* b_vals;
     const int32_t* csize;
-    const int32_t* csi;
-    const uint32_t* cs;
+    const int2* cpair;   // compressed B: {word index, bits} in B's own slots
     // rows
     const int32_t* list; // nullptr: rows [0, nrows)
     int64_t nrows;
@@ -79,7 +78,7 @@ struct RowLaunch {
 
 // kernel launchers (kk_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
-                            int32_t* csize, int32_t* csi, uint32_t* cs, cudaStream_t st);
+                            int32_t* csize, int2* cp, cudaStream_t st);
 cudaError_t launch_flops(int32_t m, double avg_len, const int64_t* a_rowptr,
                          const int32_t* a_cols, const int64_t* b_rowptr, const int32_t* csize,
                          int64_t* out_f, int64_t* out_cf, Totals* tot, cudaStream_t st);

@@ -86,14 +86,13 @@ __device__ __forceinline__ uint32_t group_or(uint32_t grp, uint32_t v, int lane)
 constexpr int32_t kShortRow = 8;
 
 // Thread per B row for rows of <= kShortRow entries:
-// the running (csi, cs) pair stays in registers and is flushed when the word
+// the running (word index, bits) pair stays in registers and is flushed when the word
 // changes; an out-of-order word (unsorted row) merges into its earlier pair.
 // Longer rows are left to the warp kernel below.
 __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                              const int32_t* __restrict__ cols,
                                                              int32_t* __restrict__ csize,
-                                                             int32_t* __restrict__ csi,
-                                                             uint32_t* __restrict__ cs)
+                                                             int2* __restrict__ cp)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += stride) { // warp-uniform trips
@@ -121,33 +120,32 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const in
             int32_t found = -1;
             if (w <= maxw) // not beyond every word seen so far: maybe an earlier pair
                 for (int32_t t = 0; t < np; ++t)
-                    if (csi[lo + t] == w) {
+                    if (cp[lo + t].x == w) {
                         found = t;
                         break;
                     }
             if (cur_w >= 0) { // flush the running pair
-                cs[lo + np - 1] = cur;
+                cp[lo + np - 1].y = static_cast<int>(cur);
                 cur_w = -1;
             }
             if (found >= 0) { // merge into the earlier pair, in place (first-touch order kept)
-                cs[lo + found] |= bit;
+                cp[lo + found].y |= static_cast<int>(bit);
                 continue;
             }
-            csi[lo + np] = w;
+            cp[lo + np].x = w;
             ++np;
             cur_w = w;
             cur = bit;
             maxw = max(maxw, w);
         }
         if (cur_w >= 0)
-            cs[lo + np - 1] = cur;
+            cp[lo + np - 1].y = static_cast<int>(cur);
         csize[j] = np;
     }
 }
 
 __device__ __forceinline__ void compress_row_short(int64_t j, int64_t lo, int64_t len, int32_t col, int lane,
-                                                   int32_t* __restrict__ csize, int32_t* __restrict__ csi,
-                                                   uint32_t* __restrict__ cs)
+                                                   int32_t* __restrict__ csize, int2* __restrict__ cp)
 {
     const bool valid = lane < len;
     const int32_t w = col >> 5;
@@ -156,17 +154,14 @@ __device__ __forceinline__ void compress_row_short(int64_t j, int64_t lo, int64_
     const uint32_t orv = group_or(grp, valid ? (1u << (col & 31)) : 0u, lane);
     const bool leader = valid && (__ffs(grp) - 1) == lane;
     const uint32_t lm = __ballot_sync(kFull, leader);
-    if (leader) {
-        const int pos = __popc(lm & lanemask_lt());
-        csi[lo + pos] = w;
-        cs[lo + pos] = orv;
-    }
+    if (leader)
+        cp[lo + __popc(lm & lanemask_lt())] = make_int2(w, static_cast<int>(orv));
     if (lane == 0)
         csize[j] = __popc(lm);
 }
 
 __device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
-                                  int32_t* __restrict__ csize, int32_t* __restrict__ csi, uint32_t* __restrict__ cs);
+                                  int32_t* __restrict__ csize, int2* __restrict__ cp);
 
 // Warp kernel for rows of more than kShortRow entries.  A warp takes batches
 // of 32 consecutive rows: one coalesced load of their offsets, then the long
@@ -175,8 +170,7 @@ __device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int3
 __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ cols,
                                                        int32_t* __restrict__ csize,
-                                                       int32_t* __restrict__ csi,
-                                                       uint32_t* __restrict__ cs)
+                                                       int2* __restrict__ cp)
 {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -202,9 +196,9 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
         };
         auto process = [&](int q, int64_t lo, int64_t len, int32_t col) {
             if (len <= 32)
-                compress_row_short(r0 + q, lo, len, col, lane, csize, csi, cs);
+                compress_row_short(r0 + q, lo, len, col, lane, csize, cp);
             else
-                compress_row_long(r0 + q, lo, len, cols, lane, csize, csi, cs);
+                compress_row_long(r0 + q, lo, len, cols, lane, csize, cp);
         };
         int64_t loA = 0, lenA = 0, loB = 0, lenB = 0;
         int32_t colA = 0, colB = 0;
@@ -227,7 +221,7 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
 }
 
 __device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
-                                  int32_t* __restrict__ csize, int32_t* __restrict__ csi, uint32_t* __restrict__ cs)
+                                  int32_t* __restrict__ csize, int2* __restrict__ cp)
 {
     {
         // long row: sortedness first (one extra read of the row, L1/L2 resident)
@@ -257,13 +251,10 @@ __device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int3
                     pw = carry_w;
                 const bool start = valid && w != pw;
                 if (valid && lane == 0 && w == carry_w)
-                    cs[lo + cnt - 1] |= orv; // run continues from the previous chunk
+                    cp[lo + cnt - 1].y |= static_cast<int>(orv); // run continues from the previous chunk
                 const uint32_t lm = __ballot_sync(kFull, start);
-                if (start) {
-                    const int pos = cnt + __popc(lm & lanemask_lt());
-                    csi[lo + pos] = w;
-                    cs[lo + pos] = orv;
-                }
+                if (start)
+                    cp[lo + cnt + __popc(lm & lanemask_lt())] = make_int2(w, static_cast<int>(orv));
                 cnt += __popc(lm);
                 const int last = static_cast<int>(len - 1 - t0 < 31 ? len - 1 - t0 : 31);
                 carry_w = __shfl_sync(kFull, w, last);
@@ -281,20 +272,17 @@ __device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int3
                 int32_t found = -1;
                 if (leader)
                     for (int32_t q = 0; q < cnt; ++q)
-                        if (csi[lo + q] == w) {
+                        if (cp[lo + q].x == w) {
                             found = q;
                             break;
                         }
                 __syncwarp();
                 const bool is_new = leader && found < 0;
                 const uint32_t nm = __ballot_sync(kFull, is_new);
-                if (is_new) {
-                    const int pos = cnt + __popc(nm & lanemask_lt());
-                    csi[lo + pos] = w;
-                    cs[lo + pos] = orv;
-                } else if (leader) {
-                    cs[lo + found] |= orv;
-                }
+                if (is_new)
+                    cp[lo + cnt + __popc(nm & lanemask_lt())] = make_int2(w, static_cast<int>(orv));
+                else if (leader)
+                    cp[lo + found].y |= static_cast<int>(orv);
                 cnt += __popc(nm);
                 __syncwarp();
             }
@@ -562,7 +550,7 @@ __global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
             cnt = warp_row<kFlat, true>(L.a_rowptr, L.a_cols, nullptr, i, src, map, ids, pay,
                                         cap, L.ctr, lane, products);
         } else {
-            const CompressedSource src{L.b_rowptr, L.csize, L.csi, L.cs};
+            const CompressedSource src{L.b_rowptr, L.csize, L.cpair};
             cnt = warp_row<kFlat, false>(L.a_rowptr, L.a_cols, nullptr, i, src, map, ids, pay,
                                          cap, L.ctr, lane, products);
         }
@@ -944,17 +932,17 @@ cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, do
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
-                            int32_t* csize, int32_t* csi, uint32_t* cs, cudaStream_t st)
+                            int32_t* csize, int2* cp, cudaStream_t st)
 {
     if (n <= 0)
         return cudaSuccess;
     // short rows: thread per row; longer rows: warp per row in batches of 32
     const int tblocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
-    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs);
+    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp);
     count_launch();
     const int64_t batches = (n + 31) / 32;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((batches + 7) / 8, (int64_t)sm_count() * 8));
-    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, csi, cs);
+    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp);
     count_launch();
     return cudaGetLastError();
 }
