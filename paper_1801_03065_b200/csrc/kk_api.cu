@@ -854,10 +854,15 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         cuda_check(cudaMemcpyAsync(hviews + 1, a->row_offsets + m, 8, cudaMemcpyDeviceToHost, st), "A view");
         cuda_check(cudaMemcpyAsync(hviews + 2, b->row_offsets, 8, cudaMemcpyDeviceToHost, st), "B view");
         cuda_check(cudaMemcpyAsync(hviews + 3, b->row_offsets + n, 8, cudaMemcpyDeviceToHost, st), "B view");
-        // the band of B rows A references (only those are compressed)
+        // the band of B rows A references, when A is at most half as tall as
+        // B (a row shard): only that band is compressed
         int* hcrange = reinterpret_cast<int*>(hviews + 8);
-        cuda_check(launch_col_range(m, a->row_offsets, a->col_indices, d_crange, st), "column range");
-        cuda_check(cudaMemcpyAsync(hcrange, d_crange, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "column range");
+        hcrange[0] = 0;
+        hcrange[1] = n - 1;
+        if (int64_t{m} * 2 <= n) {
+            cuda_check(launch_col_range(m, a->row_offsets, a->col_indices, d_crange, st), "column range");
+            cuda_check(cudaMemcpyAsync(hcrange, d_crange, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "column range");
+        }
         cuda_check(cudaEventRecord(ev[0], st), "event");
         cuda_check(cudaMemsetAsync(d_tot, 0, sizeof(Totals), st), "memset");
         cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");

@@ -313,47 +313,65 @@ __global__ void __launch_bounds__(256) flops_kernel(int32_t m, const int64_t* __
     const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
     unsigned long long my_tf = 0, my_mf = 0, my_tcf = 0, my_mcf = 0;
     const int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
-    // uniform trip count per warp so the group shuffles stay converged
-    const int64_t iters = (m + groups - 1) / groups;
+    // uniform trip count per warp so the group shuffles stay converged; two
+    // rows per group per trip, their loads issued together (the chain
+    // row offsets -> A columns -> B offsets is latency-bound)
+    const int64_t iters = (m + 2 * groups - 1) / (2 * groups);
     for (int64_t it = 0; it < iters; ++it) {
-        const int64_t i = first + it * groups;
-        int64_t f = 0, cf = 0;
-        if (i < m) {
-            const int64_t beg = __ldg(a_rowptr + i), end = __ldg(a_rowptr + i + 1);
-            int64_t p = beg + glane;
-            for (; p + 3 * G < end; p += 4 * G) {
+        int64_t i2[2], beg[2], end[2], f2[2] = {0, 0}, cf2[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            i2[u] = first + (2 * it + u) * groups;
+            beg[u] = end[u] = 0;
+            if (i2[u] < m) {
+                beg[u] = __ldg(a_rowptr + i2[u]);
+                end[u] = __ldg(a_rowptr + i2[u] + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            int64_t p = beg[u] + glane;
+            int64_t f = 0, cf = 0;
+            for (; p + 3 * G < end[u]; p += 4 * G) {
                 int32_t j[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    j[u] = __ldg(a_cols + p + u * G);
+                for (int v = 0; v < 4; ++v)
+                    j[v] = __ldg(a_cols + p + v * G);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    f += __ldg(b_rowptr + j[u] + 1) - __ldg(b_rowptr + j[u]);
-                    cf += __ldg(csize + j[u]);
+                for (int v = 0; v < 4; ++v) {
+                    f += __ldg(b_rowptr + j[v] + 1) - __ldg(b_rowptr + j[v]);
+                    cf += __ldg(csize + j[v]);
                 }
             }
-            for (; p < end; p += G) {
+            for (; p < end[u]; p += G) {
                 const int32_t j = __ldg(a_cols + p);
                 f += __ldg(b_rowptr + j + 1) - __ldg(b_rowptr + j);
                 cf += __ldg(csize + j);
             }
+            f2[u] = f;
+            cf2[u] = cf;
         }
 #pragma unroll
-        for (int off = G / 2; off >= 1; off >>= 1) {
-            f += __shfl_xor_sync(kFull, f, off, G);
-            cf += __shfl_xor_sync(kFull, cf, off, G);
+        for (int u = 0; u < 2; ++u) {
+            int64_t f = f2[u], cf = cf2[u];
+            const int64_t i = i2[u];
+#pragma unroll
+            for (int off = G / 2; off >= 1; off >>= 1) {
+                f += __shfl_xor_sync(kFull, f, off, G);
+                cf += __shfl_xor_sync(kFull, cf, off, G);
+            }
+            const bool owner = glane == 0 && i < m;
+            if (owner) {
+                out_f[i] = f;
+                out_cf[i] = cf;
+                my_tf += f;
+                my_tcf += cf;
+                my_mf = max(my_mf, (unsigned long long)f);
+                my_mcf = max(my_mcf, (unsigned long long)cf);
+            }
+            warp_hist_add(sh_hist[0], owner ? bucket_of(f) : -1, threadIdx.x & 31);
+            warp_hist_add(sh_hist[1], owner ? bucket_of(cf) : -1, threadIdx.x & 31);
         }
-        const bool owner = glane == 0 && i < m;
-        if (owner) {
-            out_f[i] = f;
-            out_cf[i] = cf;
-            my_tf += f;
-            my_tcf += cf;
-            my_mf = max(my_mf, (unsigned long long)f);
-            my_mcf = max(my_mcf, (unsigned long long)cf);
-        }
-        warp_hist_add(sh_hist[0], owner ? bucket_of(f) : -1, threadIdx.x & 31);
-        warp_hist_add(sh_hist[1], owner ? bucket_of(cf) : -1, threadIdx.x & 31);
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
