@@ -392,6 +392,7 @@ def main():
         "roofline_replay": None if replay_state != 2 else {
             "bound": "hbm", "achieved": replay_bytes / (replay_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": replay_bytes / (replay_ms / 1e3) / 1e9 / hbm, "kernel": "replay_numeric_kernel (+ structure fingerprint pass)",
+            "traffic": load_traffic(f"c{args.config}_replay"),
             "algorithmic_bytes": replay_bytes, "model": "24(m+1)+28nnzA+(8+w)flops+16nnzC, w = slot bytes"},
         "cpu_baseline": cpu,
         "e2e": e2e,
