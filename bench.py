@@ -361,6 +361,7 @@ def main():
         return
 
     peaks, peak_kind = _peaks()
+    full_size = args.scale == 1.0 and world == 1  # the committed ncu traffic is for this workload
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     bytes_num = algorithmic_bytes_numeric(hi - lo, nnz_a if world == 1 else info.nnz_a, flops_local, nnz_c_local)
     achieved = bytes_num / (num_kernel_ms / 1e3) / 1e9
@@ -385,14 +386,15 @@ def main():
                          "hashing_kernels": {"value": 2.0 * flops / (ms_hash / 1e3) / 1e9, "unit": UNIT,
                                              "ms_per_step": ms_hash}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": load_traffic(f"c{args.config}_numeric"),
+                     "frac": achieved / hbm,
+                     "traffic": load_traffic(f"c{args.config}_numeric") if full_size else None,
                      "kernel": "numeric_lp_seq_kernel (numeric phase)", "peak_kind": peak_kind,
                      "algorithmic_bytes": bytes_num,
                      "model": "16(m+1)+28nnzA+12flops+12nnzC (SURVEY §8d)"},
         "roofline_replay": None if replay_state != 2 else {
             "bound": "hbm", "achieved": replay_bytes / (replay_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": replay_bytes / (replay_ms / 1e3) / 1e9 / hbm, "kernel": "replay_numeric_kernel (+ structure fingerprint pass)",
-            "traffic": load_traffic(f"c{args.config}_replay"),
+            "traffic": load_traffic(f"c{args.config}_replay") if full_size else None,
             "algorithmic_bytes": replay_bytes, "model": "24(m+1)+28nnzA+(8+w)flops+16nnzC, w = slot bytes"},
         "cpu_baseline": cpu,
         "e2e": e2e,
