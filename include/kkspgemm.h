@@ -215,6 +215,13 @@ void spg_handle_destroy(spg_handle_t h);
 int spg_sort_rows(int32_t m, const int64_t* d_row_offsets, int32_t* d_cols, double* d_vals,
                   void* stream);
 
+/* Transpose of a device CSR (csr_matrix.cpp:82-108: entries of each result
+ * row in increasing original-row order) into caller buffers: d_t_row_offsets
+ * [a->num_cols + 1], d_t_cols/d_t_vals [a->nnz].  Used for R = P^T of the
+ * multigrid triple product.  Synchronises once (the longest result row). */
+int spg_transpose(const spg_csr* a, int64_t* d_t_row_offsets, int32_t* d_t_cols, double* d_t_vals,
+                  void* stream);
+
 /* Per-row multiplication counts (flops_stats per_row_flops, csr_matrix.cpp:136-154)
  * into device memory d_out[a->num_rows]; stream-ordered.  Used for the
  * flop-balanced row partition of the multi-GPU path. */

@@ -176,7 +176,7 @@ class Reference:
                 raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference)")
         L = C.CDLL(REF_SO)
         for f in ("ref_mat_new", "ref_build_csr", "ref_transpose", "ref_generate_synthetic", "ref_rng_new",
-                  "ref_random_csr", "ref_shuffle_rows", "ref_synthetic_by_index", "ref_symbolic"):
+                  "ref_random_csr", "ref_shuffle_rows", "ref_synthetic_by_index", "ref_symbolic", "ref_read_mm"):
             getattr(L, f).restype = _P
         L.ref_mat_new.argtypes = [C.c_int32, C.c_int32, _P, _P, _P, C.c_int]
         L.ref_mat_free.argtypes = [_P]
@@ -184,6 +184,7 @@ class Reference:
         L.ref_mat_export.argtypes = [_P, _P, _P, _P]
         L.ref_build_csr.argtypes = [C.c_int32, C.c_int32, C.c_int64, _P, _P, _P]
         L.ref_transpose.argtypes = [_P]
+        L.ref_read_mm.argtypes = [C.c_char_p]
         L.ref_generate_synthetic.argtypes = [C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_uint64]
         L.ref_rng_new.argtypes = [C.c_uint64]
         L.ref_rng_free.argtypes = [_P]
@@ -218,6 +219,16 @@ class Reference:
         v = np.ascontiguousarray(m.values, np.float64)
         return RefMat(self, self.L.ref_mat_new(m.num_rows, m.num_cols, _ptr(ro), _ptr(ci), _ptr(v),
                                                int(bool(m.sorted_rows))))
+
+    def read_mm(self, path: str):
+        """The reference's read_matrix_market (matrix_market.cpp:48-132)."""
+        ptr = self.L.ref_read_mm(str(path).encode())
+        if not ptr:
+            raise ValueError(self.L.ref_last_error().decode())
+        try:
+            return self.export(ptr)
+        finally:
+            self.L.ref_mat_free(ptr)
 
     def export(self, handle):
         from paper_1801_03065_b200 import CsrMatrix

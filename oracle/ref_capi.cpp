@@ -22,6 +22,7 @@
 #include "spgemm/compression.hpp"
 #include "spgemm/csr_matrix.hpp"
 #include "spgemm/engine.hpp"
+#include "spgemm/matrix_market.hpp"
 #include "spgemm/oracle.hpp"
 #include "spgemm/synthetic.hpp"
 #include "test_util.hpp"
@@ -158,6 +159,14 @@ void* ref_mat_new(int32_t rows, int32_t cols, const int64_t* rowptr, const int32
 }
 
 void ref_mat_free(void* m) { delete static_cast<CsrMatrix*>(m); }
+
+// the reference's MatrixMarket reader (matrix_market.cpp); NULL on error
+void* ref_read_mm(const char* path)
+{
+    CsrMatrix* out = nullptr;
+    const int rc = guard([&] { out = new CsrMatrix(read_matrix_market(path, nullptr)); });
+    return rc == 0 ? out : nullptr;
+}
 
 void ref_mat_shape(void* mp, int32_t* rows, int32_t* cols, int64_t* nnz)
 {

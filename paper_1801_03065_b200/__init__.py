@@ -158,7 +158,7 @@ EXPORTED_SYMBOLS = (
     "spg_symbolic", "spg_numeric", "spg_handle_info_get", "spg_handle_copy_row_offsets",
     "spg_handle_copy_per_row_flops", "spg_handle_copy_row_offsets_device", "spg_handle_set_numeric", "spg_handle_import",
     "spg_handle_check", "spg_handle_destroy", "spg_sort_rows", "spg_kernel_launch_count",
-    "spg_row_flops", "spg_handle_replay_state", "spg_numeric_rows",
+    "spg_row_flops", "spg_handle_replay_state", "spg_numeric_rows", "spg_transpose",
 )
 
 _lib_handle = None
@@ -176,6 +176,8 @@ def lib() -> C.CDLL:
         L.spg_kernel_launch_count.restype = C.c_int64
         L.spg_handle_destroy.restype = None
         L.spg_handle_replay_state.restype = C.c_int
+        L.spg_transpose.restype = C.c_int
+        L.spg_transpose.argtypes = [C.POINTER(_Csr), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.spg_handle_replay_state.argtypes = [C.c_void_p]
         for name in ("spg_config_init", "spg_resolve_config", "spg_flat_position", "spg_symbolic",
                      "spg_numeric", "spg_handle_info_get", "spg_handle_copy_row_offsets",
@@ -594,6 +596,19 @@ def row_flops(a, b, stream=None):
     out = torch.empty(max(da.num_rows, 1), dtype=torch.int64, device=da.row_offsets.device)
     _check(lib().spg_row_flops(C.byref(da._c()), C.byref(db._c()), out.data_ptr(), _stream_ptr(stream)))
     return out[:da.num_rows]
+
+
+def transpose(a, stream=None) -> DeviceCsr:
+    """A^T on the device (csr_matrix.cpp:82-108 order), e.g. R = P^T."""
+    import torch
+    da = _dev(a)
+    dev = da.row_offsets.device
+    nnz = da.nnz()
+    ro = torch.empty(da.num_cols + 1, dtype=torch.int64, device=dev)
+    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    v = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    _check(lib().spg_transpose(C.byref(da._c()), ro.data_ptr(), ci.data_ptr(), v.data_ptr(), _stream_ptr(stream)))
+    return DeviceCsr(da.num_cols, da.num_rows, ro, ci[:nnz], v[:nnz], True, nnz)
 
 
 def sort_rows(c: DeviceCsr, stream=None) -> DeviceCsr:

@@ -11,9 +11,21 @@
 //   aggregation piecewise-constant 2x2x2 aggregation prolongator P (1 nnz/row, value 1)
 // Stencil weights are perturbed w*(1 + eps*U(-1,1)) from mt19937_64(seed) in CSR
 // order so the 1e-12 value check has power (SURVEY.md §8c caveat).
+//
+// kkg_read_mm: MatrixMarket ingest with the reference reader's contract
+// (matrix_market.cpp:48-132): coordinate real/integer/pattern, general or
+// symmetric (mirrored off-diagonal entries), 1-based indices checked against
+// the size line, '%' comment and blank lines skipped, entries through the
+// same build_csr semantics (duplicates summed in encounter order).
 #include <algorithm>
+#include <cerrno>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <limits>
+#include <sstream>
+#include <string>
 #include <numeric>
 #include <random>
 #include <vector>
@@ -82,9 +94,126 @@ Mat build(int32_t rows, int32_t cols, const std::vector<int32_t>& r, const std::
     return m;
 }
 
+bool blank(const std::string& s)
+{
+    for (char c : s)
+        if (c != ' ' && c != '\t' && c != '\r' && c != '\n' && c != '\f' && c != '\v')
+            return false;
+    return true;
+}
+
+struct MmError {
+    std::string what;
+    long line;
+};
+
+long long mm_int(const char*& p, long line, const char* what)
+{
+    errno = 0;
+    char* end = nullptr;
+    const long long v = std::strtoll(p, &end, 10);
+    if (end == p || errno == ERANGE)
+        throw MmError{std::string("expected ") + what, line};
+    p = end;
+    return v;
+}
+
+Mat read_mm(const char* path)
+{
+    std::ifstream in(path);
+    if (!in)
+        throw MmError{std::string("cannot open '") + path + "' for reading", 0};
+    std::string ln;
+    long line = 0;
+    if (!std::getline(in, ln))
+        throw MmError{"missing MatrixMarket header", 1};
+    ++line;
+    std::istringstream hdr(ln);
+    std::string banner, object, format, field, symmetry;
+    hdr >> banner >> object >> format >> field >> symmetry;
+    if (banner != "%%MatrixMarket" || object != "matrix")
+        throw MmError{"not a MatrixMarket matrix header", line};
+    if (format != "coordinate")
+        throw MmError{"only coordinate format is supported", line};
+    const bool pattern = field == "pattern";
+    if (!pattern && field != "real" && field != "integer")
+        throw MmError{"unsupported field '" + field + "'", line};
+    const bool symmetric = symmetry == "symmetric";
+    if (!symmetric && symmetry != "general")
+        throw MmError{"unsupported symmetry '" + symmetry + "'", line};
+    long long rows = 0, cols = 0, entries = 0;
+    for (;;) {
+        if (!std::getline(in, ln))
+            throw MmError{"missing size line", line + 1};
+        ++line;
+        if ((!ln.empty() && ln[0] == '%') || blank(ln))
+            continue;
+        const char* p = ln.c_str();
+        rows = mm_int(p, line, "row count");
+        cols = mm_int(p, line, "column count");
+        entries = mm_int(p, line, "entry count");
+        break;
+    }
+    if (rows < 0 || cols < 0 || entries < 0)
+        throw MmError{"negative size field", line};
+    const long long imax = std::numeric_limits<int32_t>::max();
+    if (rows > imax || cols > imax || entries > imax)
+        throw MmError{"size exceeds 32-bit index range", line};
+    std::vector<int32_t> r, c;
+    std::vector<double> v;
+    r.reserve(static_cast<size_t>(symmetric ? 2 * entries : entries));
+    c.reserve(r.capacity());
+    v.reserve(r.capacity());
+    for (long long seen = 0; seen < entries;) {
+        if (!std::getline(in, ln))
+            throw MmError{"unexpected end of file: " + std::to_string(entries - seen) + " entries missing", line + 1};
+        ++line;
+        if ((!ln.empty() && ln[0] == '%') || blank(ln))
+            continue;
+        const char* p = ln.c_str();
+        const long long ri = mm_int(p, line, "row index");
+        const long long ci = mm_int(p, line, "column index");
+        if (ri < 1 || ri > rows || ci < 1 || ci > cols)
+            throw MmError{"index out of range", line};
+        double x = 1.0;
+        if (!pattern) {
+            char* end = nullptr;
+            x = std::strtod(p, &end);
+            if (end == p)
+                throw MmError{"expected a numeric value", line};
+        }
+        r.push_back(static_cast<int32_t>(ri - 1));
+        c.push_back(static_cast<int32_t>(ci - 1));
+        v.push_back(x);
+        if (symmetric && ri != ci) {
+            r.push_back(static_cast<int32_t>(ci - 1));
+            c.push_back(static_cast<int32_t>(ri - 1));
+            v.push_back(x);
+        }
+        ++seen;
+    }
+    return build(static_cast<int32_t>(rows), static_cast<int32_t>(cols), r, c, v);
+}
+
 } // namespace
 
 extern "C" {
+
+// MatrixMarket ingest; NULL on error with the message (and 1-based line, 0 if
+// none) in err[0..errlen)
+void* kkg_read_mm(const char* path, char* err, int32_t errlen)
+{
+    try {
+        return new Mat(read_mm(path));
+    } catch (const MmError& e) {
+        const std::string msg = e.line > 0 ? e.what + " (line " + std::to_string(e.line) + ")" : e.what;
+        if (err && errlen > 0) {
+            std::strncpy(err, msg.c_str(), static_cast<size_t>(errlen) - 1);
+            err[errlen - 1] = 0;
+        }
+        return nullptr;
+    }
+}
 
 void* kkg_laplace2d(int32_t n, double eps, uint64_t seed)
 {

@@ -1357,6 +1357,29 @@ int spg_row_flops(const spg_csr* a, const spg_csr* b, int64_t* d_out, void* stre
     });
 }
 
+int spg_transpose(const spg_csr* a, int64_t* d_t_row_offsets, int32_t* d_t_cols, double* d_t_vals, void* stream)
+{
+    return guarded([&] {
+        validate_csr(a, "transpose: A", true);
+        if (!d_t_row_offsets || (a->nnz > 0 && (!d_t_cols || !d_t_vals)))
+            fail(SPG_ERR_CONTRACT, "transpose: null output");
+        require_device();
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        ScanTotals* d_stot = dalloc<ScanTotals>(1, st, "scan totals");
+        ScanTotals hs{};
+        cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");
+        cuda_check(launch_transpose_count(a->num_rows, a->num_cols, a->row_offsets, a->col_indices, d_t_row_offsets,
+                                          d_stot, st),
+                   "transpose count");
+        cuda_check(cudaMemcpyAsync(&hs, d_stot, sizeof(hs), cudaMemcpyDeviceToHost, st), "transpose totals");
+        cuda_check(cudaStreamSynchronize(st), "transpose sync");
+        cudaFreeAsync(d_stot, st);
+        cuda_check(launch_transpose_fill(a->num_rows, a->num_cols, a->row_offsets, a->col_indices, a->values,
+                                         d_t_row_offsets, d_t_cols, d_t_vals, static_cast<int64_t>(hs.max_size), st),
+                   "transpose fill");
+    });
+}
+
 int spg_sort_rows(int32_t m, const int64_t* d_row_offsets, int32_t* d_cols, double* d_vals, void* stream)
 {
     return guarded([&] {

@@ -98,6 +98,11 @@ cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, do
                              int64_t max_row, cudaStream_t st);
 cudaError_t launch_row_flops(int32_t m, const int64_t* a_rowptr, const int32_t* a_cols,
                              const int64_t* b_rowptr, int64_t* out, cudaStream_t st);
+cudaError_t launch_transpose_count(int32_t m, int32_t n, const int64_t* rowptr, const int32_t* cols,
+                                   int64_t* t_rowptr, ScanTotals* tot, cudaStream_t st);
+cudaError_t launch_transpose_fill(int32_t m, int32_t n, const int64_t* rowptr, const int32_t* cols,
+                                  const double* vals, const int64_t* t_rowptr, int32_t* t_cols, double* t_vals,
+                                  int64_t max_row, cudaStream_t st);
 cudaError_t launch_col_range(int32_t m, const int64_t* a_rowptr, const int32_t* a_cols, int* out2, cudaStream_t st);
 cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals* tot,
                                    cudaStream_t st);

@@ -788,6 +788,77 @@ cudaError_t launch_col_range(int32_t m, const int64_t* a_rowptr, const int32_t* 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Transpose (csr_matrix.cpp:82-108): column counts, in-place scan, scatter
+// through per-column cursors, then the rows of the result are sorted by
+// their (original row) column index, which restores the reference's order
+// (entries of a column in increasing row order).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) transpose_count_kernel(int32_t m, const int64_t* __restrict__ rowptr,
+                                                              const int32_t* __restrict__ cols,
+                                                              unsigned long long* __restrict__ cnt)
+{
+    const int64_t lo = __ldg(rowptr), hi = __ldg(rowptr + m);
+    for (int64_t q = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + __ldg(cols + q), 1ull);
+}
+
+__global__ void __launch_bounds__(256) transpose_scatter_kernel(int32_t m, const int64_t* __restrict__ rowptr,
+                                                                const int32_t* __restrict__ cols,
+                                                                const double* __restrict__ vals,
+                                                                unsigned long long* __restrict__ cursor,
+                                                                int32_t* __restrict__ t_cols, double* __restrict__ t_vals)
+{
+    // warp per row: the row index is the transposed entry's column
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
+        const int64_t lo = __ldg(rowptr + i), hi = __ldg(rowptr + i + 1);
+        for (int64_t q = lo + lane; q < hi; q += 32) {
+            const unsigned long long p = atomicAdd(cursor + __ldg(cols + q), 1ull);
+            t_cols[p] = static_cast<int32_t>(i);
+            if (vals)
+                t_vals[p] = __ldg(vals + q);
+        }
+    }
+}
+
+// phase 1: column counts -> t_rowptr (scanned); tot->max_size = longest row of A^T
+cudaError_t launch_transpose_count(int32_t m, int32_t n, const int64_t* rowptr, const int32_t* cols,
+                                   int64_t* t_rowptr, ScanTotals* tot, cudaStream_t st)
+{
+    cudaError_t e = cudaMemsetAsync(t_rowptr, 0, sizeof(int64_t) * (static_cast<size_t>(n) + 1), st);
+    if (e != cudaSuccess)
+        return e;
+    if (m > 0) {
+        transpose_count_kernel<<<sm_count() * 4, 256, 0, st>>>(m, rowptr, cols,
+                                                              reinterpret_cast<unsigned long long*>(t_rowptr + 1));
+        count_launch();
+    }
+    return scan_sizes_inplace(t_rowptr, n, tot, st);
+}
+
+// phase 2: scatter through per-column cursors, then sort the rows of A^T
+cudaError_t launch_transpose_fill(int32_t m, int32_t n, const int64_t* rowptr, const int32_t* cols,
+                                  const double* vals, const int64_t* t_rowptr, int32_t* t_cols, double* t_vals,
+                                  int64_t max_row, cudaStream_t st)
+{
+    if (m <= 0)
+        return cudaSuccess;
+    unsigned long long* cursor = nullptr;
+    cudaError_t e = cudaMallocAsync(&cursor, sizeof(int64_t) * (static_cast<size_t>(n) + 1), st);
+    if (e != cudaSuccess)
+        return e;
+    cudaMemcpyAsync(cursor, t_rowptr, sizeof(int64_t) * (static_cast<size_t>(n) + 1), cudaMemcpyDeviceToDevice, st);
+    const int blocks = static_cast<int>(std::min<int64_t>((m + 7) / 8, (int64_t)sm_count() * 8));
+    transpose_scatter_kernel<<<blocks, 256, 0, st>>>(m, rowptr, cols, vals, cursor, t_cols, t_vals);
+    count_launch();
+    cudaFreeAsync(cursor, st);
+    if ((e = cudaGetLastError()) != cudaSuccess)
+        return e;
+    return launch_sort_rows(n, t_rowptr, t_cols, t_vals, max_row, st);
+}
+
 // per-row flops only (K1 without compression): the flop-balanced row
 // partition of the multi-GPU path.  Warp per row.
 __global__ void __launch_bounds__(256) row_flops_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,

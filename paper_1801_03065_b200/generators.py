@@ -20,8 +20,10 @@ def _g():
             from .build import build_generators
             build_generators()
         L = C.CDLL(GEN_PATH)
-        for f in ("kkg_laplace2d", "kkg_laplace3d", "kkg_rmat", "kkg_aggregation", "kkg_transpose"):
+        for f in ("kkg_laplace2d", "kkg_laplace3d", "kkg_rmat", "kkg_aggregation", "kkg_transpose",
+                  "kkg_read_mm"):
             getattr(L, f).restype = C.c_void_p
+        L.kkg_read_mm.argtypes = [C.c_char_p, C.c_char_p, C.c_int32]
         L.kkg_laplace2d.argtypes = [C.c_int32, C.c_double, C.c_uint64]
         L.kkg_laplace3d.argtypes = [C.c_int32, C.c_double, C.c_uint64]
         L.kkg_rmat.argtypes = [C.c_int32, C.c_int32, C.c_uint64]
@@ -64,6 +66,28 @@ def rmat(scale: int, edge_factor: int = 16, seed: int = 1) -> CsrMatrix:
 def aggregation(n: int) -> CsrMatrix:
     """Piecewise-constant 2x2x2 aggregation prolongator for an n^3 grid."""
     return _take(_g().kkg_aggregation(n))
+
+
+def read_matrix_market(path: str) -> CsrMatrix:
+    """MatrixMarket coordinate file -> CsrMatrix (matrix_market.cpp:48-132
+    contract: real/integer/pattern, general/symmetric, duplicates summed).
+    Raises ValueError (the reference's ParseError/IoError) on bad input."""
+    err = C.create_string_buffer(512)
+    ptr = _g().kkg_read_mm(os.fsencode(path), err, len(err))
+    if not ptr:
+        raise ValueError(err.value.decode())
+    return _take(ptr)
+
+
+def write_matrix_market(m: CsrMatrix, path: str) -> None:
+    """General real coordinate file, 1-based, %.17g values (round-trips)."""
+    base = int(m.row_offsets[0]) if len(m.row_offsets) else 0
+    with open(path, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real general\n")
+        f.write(f"{m.num_rows} {m.num_cols} {m.nnz()}\n")
+        for i in range(m.num_rows):
+            for q in range(int(m.row_offsets[i]) - base, int(m.row_offsets[i + 1]) - base):
+                f.write(f"{i + 1} {int(m.col_indices[q]) + 1} {float(m.values[q]):.17g}\n")
 
 
 def transpose(m: CsrMatrix) -> CsrMatrix:

@@ -591,3 +591,27 @@ def test_numeric_reuse_is_graph_capturable(kk, oracle):
         ap = kk.CsrMatrix(a.num_rows, a.num_cols, a.row_offsets, a.col_indices, a.values * f, a.sorted_rows)
         c = kk.CsrMatrix(a.num_rows, b.num_cols, h.c_row_offsets, cols.cpu().numpy(), vals.cpu().numpy())
         assert_parity(oracle, ap, b, c)
+
+
+def test_device_transpose(kk, oracle):
+    """spg_transpose equals csr_matrix.cpp:82-108's transpose (the generators'
+    host transpose) exactly, and the device triple product R*(A*P) with the
+    device R = P^T matches the host-built one bit for bit."""
+    from paper_1801_03065_b200 import generators as G
+    rng = np.random.default_rng(71)
+    for m, n in ((1, 1), (57, 300), (400, 123)):
+        a = random_csr(rng, m, n, 0.05)
+        t = kk.transpose(a.to_device()).to_host()
+        ref = G.transpose(a)
+        assert np.array_equal(t.row_offsets, ref.row_offsets)
+        assert np.array_equal(t.col_indices, ref.col_indices)
+        assert np.array_equal(t.values.view(np.int64), ref.values.view(np.int64))
+    a, p = G.laplace3d(10), G.aggregation(10)
+    dA, dP = a.to_device(), p.to_device()
+    dR = kk.transpose(dP)
+    ap = kk.multiply(dA, dP).c
+    rap_dev = kk.multiply(dR, ap).c.to_host()
+    rap_host = kk.multiply(G.transpose(p), ap).c.to_host()
+    assert np.array_equal(rap_dev.row_offsets, rap_host.row_offsets)
+    assert np.array_equal(rap_dev.col_indices, rap_host.col_indices)
+    assert np.array_equal(rap_dev.values.view(np.int64), rap_host.values.view(np.int64))
