@@ -317,6 +317,9 @@ def main():
     ms = allmax(ms_local) / args.steps
     ms_num = allmax(ms_num_local) / args.steps
     ms_hash = allmax(ms_hash_local) / args.steps
+    # symbolic phase inside the NoReuse step = step - numeric (hashing kernels, the
+    # numeric a NoReuse multiply runs); its roofline uses SURVEY §8d bytes_sym
+    ms_sym = max(ms - ms_hash, 1e-6)
     flops = allsum(flops_local)
     nnz_c = allsum(nnz_c_local)
     value = 2.0 * flops / (ms / 1e3) / 1e9
@@ -365,6 +368,13 @@ def main():
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     bytes_num = algorithmic_bytes_numeric(hi - lo, nnz_a if world == 1 else info.nnz_a, flops_local, nnz_c_local)
     achieved = bytes_num / (num_kernel_ms / 1e3) / 1e9
+    # flops/gate pass, compress B, union over (csi, cs) pairs
+    n_b = B.num_rows
+    if info.compression.applied:
+        sym_bytes = (24 * (hi - lo + 1) + 44 * info.nnz_a + 16 * (n_b + 1) + 4 * info.nnz_b
+                     + 8 * info.compressed_nnz_b + 8 * info.compression.compressed_flops)
+    else:
+        sym_bytes = 24 * (hi - lo + 1) + 44 * info.nnz_a + 4 * flops_local
     w = 1 if info.max_row_size <= 256 else 2
     replay_bytes = (24 * (hi - lo + 1) + 28 * (nnz_a if world == 1 else info.nnz_a) + (8 + w) * flops_local
                     + 16 * nnz_c_local)
@@ -391,6 +401,11 @@ def main():
                      "kernel": "numeric_lp_seq_kernel (numeric phase)", "peak_kind": peak_kind,
                      "algorithmic_bytes": bytes_num,
                      "model": "16(m+1)+28nnzA+12flops+12nnzC (SURVEY §8d)"},
+        "roofline_symbolic": {
+            "bound": "hbm", "achieved": sym_bytes / (ms_sym / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": sym_bytes / (ms_sym / 1e3) / 1e9 / hbm, "ms_per_step": ms_sym, "algorithmic_bytes": sym_bytes,
+            "kernel": "symbolic phase (compress, flops, union, scan) = NoReuse step - hashing numeric",
+            "model": "24(m+1)+44nnzA+16(n+1)+4nnzB+8nnzBc+8cflops (compressed; SURVEY §8d)"},
         "roofline_replay": None if replay_state != 2 else {
             "bound": "hbm", "achieved": replay_bytes / (replay_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": replay_bytes / (replay_ms / 1e3) / 1e9 / hbm, "kernel": "replay_numeric_kernel (+ structure fingerprint pass)",

@@ -132,6 +132,8 @@ typedef struct spg_handle_info {
     double compress_ms;
     const int64_t* d_c_row_offsets; /* [m+1], device, owned by the handle */
     const int64_t* d_per_row_flops; /* [m], device, owned by the handle   */
+    int64_t compressed_nnz_b;       /* (word index, bits) pairs of the compressed B
+                                       rows A references (compress_rows output size) */
 } spg_handle_info;
 
 typedef struct spg_handle* spg_handle_t;

@@ -140,7 +140,8 @@ class _Info(C.Structure):
                 ("avg_row_size", C.c_double), ("avg_row_size_estimate", C.c_double),
                 ("symbolic_choice", _Resolved), ("numeric_choice", _Resolved),
                 ("config", _Config), ("symbolic_stats", _PhaseStats), ("compress_ms", C.c_double),
-                ("d_c_row_offsets", C.c_void_p), ("d_per_row_flops", C.c_void_p)]
+                ("d_c_row_offsets", C.c_void_p), ("d_per_row_flops", C.c_void_p),
+                ("compressed_nnz_b", C.c_int64)]
 
 
 class _Desc(C.Structure):

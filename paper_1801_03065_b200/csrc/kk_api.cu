@@ -879,7 +879,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         // ---- K3 + K1/K4 ----
         const int32_t j0 = std::clamp(hcrange[0], 0, n), j1 = std::clamp(hcrange[1] + 1, j0, n);
         cudaFreeAsync(d_crange, st);
-        cuda_check(launch_compress(j1 - j0, b->row_offsets + j0, b->col_indices, d_csize + j0, d_cp, st),
+        cuda_check(launch_compress(j1 - j0, b->row_offsets + j0, b->col_indices, d_csize + j0, d_cp, &d_tot->nnz_bc, st),
                    "compress");
         const double avg_len = m > 0 ? static_cast<double>(a->nnz) / m : 0.0;
         cuda_check(launch_flops(m, avg_len, a->row_offsets, a->col_indices, b->row_offsets, d_csize,
@@ -897,6 +897,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         I.avg_row_size_estimate = I.flops.avg_row_flops / std::max(cfg.collapse_divisor, 1);
         spg_compression_report& R = I.compression;
         R.compressed_flops = static_cast<int64_t>(htot->total_cf);
+        I.compressed_nnz_b = static_cast<int64_t>(htot->nnz_bc);
         R.compressed_max_row_flops = static_cast<int64_t>(htot->max_cf);
         R.cf = I.flops.total_flops > 0 ? static_cast<double>(R.compressed_flops) / I.flops.total_flops : 1.0;
         R.cmrf = I.flops.max_row_flops > 0

@@ -29,6 +29,7 @@ TabLayout make_layout(int acc, int variant, int32_t S, int32_t domain, double oc
 
 struct Totals {
     unsigned long long total_f, max_f, total_cf, max_cf;
+    unsigned long long nnz_bc; // compressed pairs written (the compress pass)
     unsigned long long hist_f[64];
     unsigned long long hist_cf[64];
 };
@@ -78,7 +79,7 @@ struct RowLaunch {
 
 // kernel launchers (kk_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
-                            int32_t* csize, int2* cp, cudaStream_t st);
+                            int32_t* csize, int2* cp, unsigned long long* nnz_bc, cudaStream_t st);
 cudaError_t launch_flops(int32_t m, double avg_len, const int64_t* a_rowptr,
                          const int32_t* a_cols, const int64_t* b_rowptr, const int32_t* csize,
                          int64_t* out_f, int64_t* out_cf, Totals* tot, cudaStream_t st);

@@ -92,9 +92,10 @@ constexpr int32_t kShortRow = 8;
 __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                              const int32_t* __restrict__ cols,
                                                              int32_t* __restrict__ csize,
-                                                             int2* __restrict__ cp)
+                                                             int2* __restrict__ cp, unsigned long long* nnz_bc)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long pairs = 0;
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += stride) { // warp-uniform trips
         const int64_t j = b0 + threadIdx.x;
         int64_t lo = 0;
@@ -141,11 +142,17 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const in
         if (cur_w >= 0)
             cp[lo + np - 1].y = static_cast<int>(cur);
         csize[j] = np;
+        pairs += static_cast<unsigned long long>(np);
     }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+        pairs += __shfl_xor_sync(kFull, pairs, off);
+    if ((threadIdx.x & 31) == 0 && pairs)
+        atomicAdd(nnz_bc, pairs);
 }
 
-__device__ __forceinline__ void compress_row_short(int64_t j, int64_t lo, int64_t len, int32_t col, int lane,
-                                                   int32_t* __restrict__ csize, int2* __restrict__ cp)
+__device__ __forceinline__ int compress_row_short(int64_t j, int64_t lo, int64_t len, int32_t col, int lane,
+                                                  int32_t* __restrict__ csize, int2* __restrict__ cp)
 {
     const bool valid = lane < len;
     const int32_t w = col >> 5;
@@ -158,10 +165,11 @@ __device__ __forceinline__ void compress_row_short(int64_t j, int64_t lo, int64_
         cp[lo + __popc(lm & lanemask_lt())] = make_int2(w, static_cast<int>(orv));
     if (lane == 0)
         csize[j] = __popc(lm);
+    return __popc(lm);
 }
 
-__device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
-                                  int32_t* __restrict__ csize, int2* __restrict__ cp);
+__device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
+                                 int32_t* __restrict__ csize, int2* __restrict__ cp);
 
 // Warp kernel for rows of more than kShortRow entries.  A warp takes batches
 // of 32 consecutive rows: one coalesced load of their offsets, then the long
@@ -170,9 +178,10 @@ __device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int3
 __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ cols,
                                                        int32_t* __restrict__ csize,
-                                                       int2* __restrict__ cp)
+                                                       int2* __restrict__ cp, unsigned long long* nnz_bc)
 {
     const int lane = threadIdx.x & 31;
+    unsigned long long pairs = 0; // warp-uniform
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < n; r0 += warps * 32) {
         const int64_t jr = r0 + lane;
@@ -196,9 +205,9 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
         };
         auto process = [&](int q, int64_t lo, int64_t len, int32_t col) {
             if (len <= 32)
-                compress_row_short(r0 + q, lo, len, col, lane, csize, cp);
+                pairs += compress_row_short(r0 + q, lo, len, col, lane, csize, cp);
             else
-                compress_row_long(r0 + q, lo, len, cols, lane, csize, cp);
+                pairs += compress_row_long(r0 + q, lo, len, cols, lane, csize, cp);
         };
         int64_t loA = 0, lenA = 0, loB = 0, lenB = 0;
         int32_t colA = 0, colB = 0;
@@ -218,10 +227,12 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
             process(qb, loB, lenB, colB);
         }
     }
+    if (lane == 0 && pairs)
+        atomicAdd(nnz_bc, pairs);
 }
 
-__device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
-                                  int32_t* __restrict__ csize, int2* __restrict__ cp)
+__device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
+                                 int32_t* __restrict__ csize, int2* __restrict__ cp)
 {
     {
         // long row: sortedness first (one extra read of the row, L1/L2 resident)
@@ -289,6 +300,7 @@ __device__ void compress_row_long(int64_t j, int64_t lo, int64_t len, const int3
         }
         if (lane == 0)
             csize[j] = cnt;
+        return cnt;
     }
 }
 
@@ -1021,17 +1033,17 @@ cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, do
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
-                            int32_t* csize, int2* cp, cudaStream_t st)
+                            int32_t* csize, int2* cp, unsigned long long* nnz_bc, cudaStream_t st)
 {
     if (n <= 0)
         return cudaSuccess;
     // short rows: thread per row; longer rows: warp per row in batches of 32
     const int tblocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
-    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp);
+    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp, nnz_bc);
     count_launch();
     const int64_t batches = (n + 31) / 32;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((batches + 7) / 8, (int64_t)sm_count() * 8));
-    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp);
+    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp, nnz_bc);
     count_launch();
     return cudaGetLastError();
 }
