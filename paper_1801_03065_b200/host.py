@@ -12,7 +12,8 @@ around the copies:
     structure only);
   * a matrix passed as both A and B (C = A*A) is uploaded once; `a_rows`
     names A as a row block of B (the row-sharded multi-GPU case) so only B
-    travels;
+    travels, and only B's row offsets plus the rows in the block's column band
+    (a shard of a banded operator needs its slab and a halo);
   * one symbolic pass over all of A (C's size is then known and, unless the
     caller passes output buffers, the pinned output comes from torch's host
     caching allocator); the numeric pass then runs in row blocks
@@ -126,12 +127,34 @@ def multiply_host(a: PinnedCsr, b: Optional[PinnedCsr] = None, cfg: Optional[Spg
         return (x.row_offsets.to(dev, non_blocking=True), x.col_indices.to(dev, non_blocking=True))
 
     mark("start", main)
-    ro_b, ci_b = up_structure(src_b)
+    b_ro_host = src_b.row_offsets.numpy()
+    band = None
+    if a_rows is not None and (lo, hi) != (0, src_b.num_rows) and hi > lo:
+        # A is rows [lo, hi) of B: only the B rows those rows reference (their
+        # column band, plus A's own rows) need to travel
+        acols = src_b.col_indices.numpy()[b_ro_host[lo]:b_ro_host[hi]]
+        if acols.size:
+            r0 = min(lo, int(acols.min()))
+            r1 = max(hi, int(acols.max()) + 1)
+            band = (r0, r1)
+    if band is None:
+        ro_b, ci_b = up_structure(src_b)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            v_b = src_b.values.to(dev, non_blocking=True)
+        h2d = src_b.nbytes()
+    else:
+        # full row offsets; columns/values of the band rows at their own offsets
+        q0, q1 = int(b_ro_host[band[0]]), int(b_ro_host[band[1]])
+        ro_b = src_b.row_offsets.to(dev, non_blocking=True)
+        ci_b = torch.empty(max(src_b.nnz(), 1), dtype=torch.int32, device=dev)
+        v_b = torch.empty(max(src_b.nnz(), 1), dtype=torch.float64, device=dev)
+        ci_b[q0:q1].copy_(src_b.col_indices[q0:q1], non_blocking=True)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            v_b[q0:q1].copy_(src_b.values[q0:q1], non_blocking=True)
+        h2d = src_b.row_offsets.numel() * 8 + (q1 - q0) * 12
     mark("structure uploaded", main)
-    side.wait_stream(main)
-    with torch.cuda.stream(side):
-        v_b = src_b.values.to(dev, non_blocking=True)
-    h2d = src_b.nbytes()
     if not same:
         ro_a, ci_a = up_structure(a)
         with torch.cuda.stream(side):

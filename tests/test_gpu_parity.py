@@ -615,3 +615,19 @@ def test_device_transpose(kk, oracle):
     assert np.array_equal(rap_dev.row_offsets, rap_host.row_offsets)
     assert np.array_equal(rap_dev.col_indices, rap_host.col_indices)
     assert np.array_equal(rap_dev.values.view(np.int64), rap_host.values.view(np.int64))
+
+
+def test_multiply_host_shard_uploads_band_only(kk, oracle):
+    """A = rows [lo, hi) of a banded B: only B's offsets and the band rows
+    travel; the product still equals the oracle's rows bit for bit."""
+    from paper_1801_03065_b200 import generators as G, host
+    a = G.laplace3d(14)
+    pa = host.PinnedCsr.from_csr(a)
+    lo, hi = 900, 1700
+    r = host.multiply_host(None, pa, a_rows=(lo, hi), blocks=2)
+    assert r.h2d_bytes < pa.nbytes() // 2
+    ro = oracle.symbolic_row_offsets(a, a)
+    cols, vals = oracle.numeric(a, a, ro)
+    assert np.array_equal(r.c.row_offsets, ro[lo:hi + 1] - ro[lo])
+    assert np.array_equal(r.c.col_indices, cols[ro[lo]:ro[hi]])
+    assert np.array_equal(r.c.values.view(np.int64), vals[ro[lo]:ro[hi]].view(np.int64))
