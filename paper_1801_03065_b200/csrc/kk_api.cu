@@ -705,11 +705,6 @@ void record_replay(spg_handle* h, const spg_csr* a, const spg_csr* b, int32_t* c
     h->replay_ready = true;
 }
 
-int64_t row_offsets_base_and_end(const spg_csr* x, int64_t* host2)
-{
-    (void)x;
-    return host2[1] - host2[0];
-}
 
 } // namespace
 
@@ -872,7 +867,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         aview[1] = hviews[1];
         bview[0] = hviews[2];
         bview[1] = hviews[3];
-        if (row_offsets_base_and_end(a, aview) != a->nnz || row_offsets_base_and_end(b, bview) != b->nnz)
+        if (aview[1] - aview[0] != a->nnz || bview[1] - bview[0] != b->nnz)
             fail(SPG_ERR_CONTRACT, "symbolic: nnz does not match row_offsets");
         int2* d_cp = d_cp_alloc - bview[0];
 
