@@ -394,52 +394,34 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
     __syncwarp();
 
     const int64_t nwarps = (int64_t)gridDim.x * L.wpb;
-    const int64_t* __restrict__ a_rowptr = L.a_rowptr;
     const int64_t* __restrict__ b_rowptr = L.b_rowptr;
 
-    for (int64_t r = (int64_t)blockIdx.x * L.wpb + wib; r < L.nrows; r += nwarps) {
-        const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
-        if (L.row_hi > 0 && (i < L.row_lo || i >= L.row_hi))
-            continue; // outside the requested row range (spg_numeric_rows)
-        const int64_t cbase = __ldg(L.c_rowptr + i);
-        const int32_t cap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - cbase);
-        if (cap == 0)
-            continue;
-        const int64_t abeg = __ldg(a_rowptr + i), aend = __ldg(a_rowptr + i + 1);
-        int32_t cnt = 0;
-        for (int64_t p0 = abeg; p0 < aend; p0 += 32) {
-            const int na = static_cast<int>(aend - p0 < 32 ? aend - p0 : 32);
-            int64_t bb = 0;
-            int32_t bl = 0;
-            double av = 0.0;
-            if (lane < na) {
-                const int32_t j = __ldg(L.a_cols + p0 + lane);
-                av = __ldg(L.a_vals + p0 + lane);
-                bb = __ldg(b_rowptr + j);
-                bl = static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
+    // One row's accumulation over a chunk of <= 32 A entries whose B-row
+    // descriptors (bb, bl) and A values are already in registers.
+    auto chunk = [&](int64_t bb, int32_t bl, double av, int32_t cap, int32_t& cnt) {
+        // flattened prefix of this chunk's B-row lengths (32-bit: one chunk of
+        // a flat-scheme row never holds 2^31 products)
+        FlatMap<true> fm;
+        fm.init(bb, bl, av, lane, scratch);
+        const int32_t total = fm.total;
+        for (int32_t w0 = 0; w0 < total; w0 += 32) {
+            const int32_t t = w0 + lane;
+            int32_t e;
+            int64_t base;
+            double a;
+            fm.window(w0, lane, e, base, a);
+            const bool valid = t < total;
+            int32_t key = 0;
+            double v = 0.0;
+            if (valid) {
+                const int64_t q = base + (t - e);
+                key = __ldg(L.b_cols + q);
+                v = __dmul_rn(a, __ldg(L.b_vals + q));
             }
-            // flattened prefix of this chunk's B-row lengths (32-bit: one
-            // chunk of a flat-scheme row never holds 2^31 products)
-            FlatMap<true> fm;
-            fm.init(bb, bl, av, lane, scratch);
-            const int32_t total = fm.total;
-            for (int32_t w0 = 0; w0 < total; w0 += 32) {
-                const int32_t t = w0 + lane;
-                int32_t e;
-                int64_t base;
-                double a;
-                fm.window(w0, lane, e, base, a);
-                const bool valid = t < total;
-                int32_t key = 0;
-                double v = 0.0;
-                if (valid) {
-                    const int64_t q = base + (t - e);
-                    key = __ldg(L.b_cols + q);
-                    v = __dmul_rn(a, __ldg(L.b_vals + q));
-                }
-                num_window(valid, key, v, keys, vals, slot_of, tmask, shift, cap, cnt, lane);
-            }
+            num_window(valid, key, v, keys, vals, slot_of, tmask, shift, cap, cnt, lane);
         }
+    };
+    auto finish = [&](int64_t cbase, int32_t cap, int32_t cnt) {
         if (cnt != cap && lane == 0)
             raise_error(L.ctr, cnt < cap ? kDevRowShort : kDevRowOverflow);
         const int32_t used = cnt < cap ? cnt : cap;
@@ -450,6 +432,111 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
             keys[s] = kEmpty;
         }
         __syncwarp();
+    };
+
+    // Rows are taken 32 at a time (one load of their A and C ranges).  Their
+    // dependent loads are software-pipelined across rows: while row k
+    // accumulates, row k+1's B-row descriptors and row k+2's A entries are in
+    // flight (three register sets, unrolled by three, so no in-flight load is
+    // copied between registers).  Rows of more than 32 A entries are walked
+    // chunk by chunk in place.
+    for (int64_t r0 = ((int64_t)blockIdx.x * L.wpb + wib) * 32; r0 < L.nrows; r0 += nwarps * 32) {
+        const int nr = static_cast<int>(L.nrows - r0 < 32 ? L.nrows - r0 : 32);
+        int64_t rab = 0, rcb = 0;
+        int32_t ralen = 0, rcap = 0;
+        if (lane < nr) {
+            const int32_t i = L.list ? __ldg(L.list + r0 + lane) : static_cast<int32_t>(r0 + lane);
+            const bool in_range = !(L.row_hi > 0 && (i < L.row_lo || i >= L.row_hi)); // spg_numeric_rows
+            if (in_range) {
+                rab = __ldg(L.a_rowptr + i);
+                ralen = static_cast<int32_t>(__ldg(L.a_rowptr + i + 1) - rab);
+                rcb = __ldg(L.c_rowptr + i);
+                rcap = static_cast<int32_t>(__ldg(L.c_rowptr + i + 1) - rcb);
+            }
+        }
+        uint32_t todo = __ballot_sync(kFull, lane < nr && rcap > 0);
+        auto pop = [&]() {
+            const int q = todo ? __ffs(todo) - 1 : -1;
+            todo &= todo - 1;
+            return q;
+        };
+        // stage 1: A entries of row q (short rows only)
+        auto s1 = [&](int q, int32_t& j, double& av) {
+            j = 0;
+            av = 0.0;
+            if (q < 0)
+                return;
+            const int32_t len = __shfl_sync(kFull, ralen, q);
+            const int64_t ab = __shfl_sync(kFull, rab, q);
+            if (len <= 32 && lane < len) {
+                j = __ldg(L.a_cols + ab + lane);
+                av = __ldg(L.a_vals + ab + lane);
+            }
+        };
+        // stage 2: B-row descriptors of row q's entries
+        auto s2 = [&](int q, int32_t j, int64_t& bb, int32_t& bl) {
+            bb = 0;
+            bl = 0;
+            if (q < 0)
+                return;
+            const int32_t len = __shfl_sync(kFull, ralen, q);
+            if (len <= 32 && lane < len) {
+                bb = __ldg(b_rowptr + j);
+                bl = static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
+            }
+        };
+        // stage 3: the row itself
+        auto s3 = [&](int q, int64_t bb, int32_t bl, double av) {
+            const int32_t len = __shfl_sync(kFull, ralen, q);
+            const int64_t cb = __shfl_sync(kFull, rcb, q);
+            const int32_t cap = __shfl_sync(kFull, rcap, q);
+            int32_t cnt = 0;
+            if (len <= 32) {
+                chunk(bb, bl, av, cap, cnt);
+            } else {
+                const int64_t ab = __shfl_sync(kFull, rab, q);
+                for (int64_t p0 = ab; p0 < ab + len; p0 += 32) {
+                    const int na = static_cast<int>(ab + len - p0 < 32 ? ab + len - p0 : 32);
+                    int64_t cbb = 0;
+                    int32_t cbl = 0;
+                    double cav = 0.0;
+                    if (lane < na) {
+                        const int32_t jj = __ldg(L.a_cols + p0 + lane);
+                        cav = __ldg(L.a_vals + p0 + lane);
+                        cbb = __ldg(b_rowptr + jj);
+                        cbl = static_cast<int32_t>(__ldg(b_rowptr + jj + 1) - cbb);
+                    }
+                    chunk(cbb, cbl, cav, cap, cnt);
+                }
+            }
+            finish(cb, cap, cnt);
+        };
+        int32_t jA, jB, jC;
+        double aA, aB, aC;
+        int64_t bA = 0, bB = 0, bC = 0;
+        int32_t lA = 0, lB = 0, lC = 0;
+        int qA = pop(), qB = pop(), qC = -1;
+        s1(qA, jA, aA);
+        s1(qB, jB, aB);
+        s2(qA, jA, bA, lA);
+        while (qA >= 0) {
+            qC = pop();
+            s1(qC, jC, aC);
+            s2(qB, jB, bB, lB);
+            s3(qA, bA, lA, aA);
+            if (qB < 0)
+                break;
+            qA = pop();
+            s1(qA, jA, aA);
+            s2(qC, jC, bC, lC);
+            s3(qB, bB, lB, aB);
+            if (qC < 0)
+                break;
+            qB = pop();
+            s1(qB, jB, aB);
+            s2(qA, jA, bA, lA);
+            s3(qC, bC, lC, aC);
+        }
     }
 }
 
