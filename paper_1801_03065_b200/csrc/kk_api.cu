@@ -202,6 +202,7 @@ struct PhasePlan {
     bool need_list = false; // more than one class: rows are binned
     L2Spec l2;
     int l2_class = -1;
+    bool short_rows = false; // symbolic fast kernel: rows pipelined 32 at a time
 };
 
 // GPU meta-algorithm (PAPER.md:849-852 and Table tab:methods): kkmem (LL,
@@ -292,11 +293,13 @@ L2Spec plan_l2(int acc, int variant, int64_t s_true, int32_t domain, int64_t row
 // optimistically at 2*bound/opt_div keys (the reference's row-size estimate
 // flops/collapse_divisor, engine.cpp:410-411, with 2x headroom).
 PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsigned long long* hist,
-                     int64_t umax, const spg_config& cfg, bool fast = false, int opt_div = 0)
+                     int64_t umax, const spg_config& cfg, bool fast = false, int opt_div = 0,
+                     bool short_rows = false)
 {
     PhasePlan P;
     P.acc = acc;
     P.flat = flat;
+    P.short_rows = short_rows;
     P.fast = fast;
     P.variant = variant;
     P.domain = domain;
@@ -372,7 +375,7 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
                 per_sm = flat ? numeric_flat_fast_blocks_per_sm(pc.wpb, smem)
                               : numeric_fast_blocks_per_sm(pc.wpb, smem);
             else
-                per_sm = symbolic_fast_blocks_per_sm(variant == kVarSymCompressed, pc.wpb, smem);
+                per_sm = symbolic_fast_blocks_per_sm(variant == kVarSymCompressed, short_rows, pc.wpb, smem);
             const int64_t want = (pc.count + pc.wpb - 1) / pc.wpb;
             pc.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sm_count())));
         } else {
@@ -925,9 +928,12 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
                       domain, raw_bound, &sacc, &sflat);
         // Auto: the order-free fast union with optimistic L1 sizing (kk_fast.cu)
         const bool sfast = cfg.accumulator == SPG_ACC_AUTO && cfg.l1_capacity <= 0;
+        // short rows (the paper's kkmem side of the avg-row-flops cutoff):
+        // latency-bound, so the fast kernel pipelines rows
+        const bool short_rows = I.flops.avg_row_flops < cfg.avg_flops_cutoff;
         const PhasePlan S = plan_phase(sfast ? kAccLP : sacc, sfast ? true : sflat, variant, domain,
                                        apply ? htot->hist_cf : htot->hist_f, raw_bound, cfg, sfast,
-                                       sfast ? std::max(cfg.collapse_divisor, 1) : 0);
+                                       sfast ? std::max(cfg.collapse_divisor, 1) : 0, short_rows);
         cuda_check(cudaMemsetAsync(h->d_rowptr, 0, sizeof(int64_t) * (int64_t{m} + 1), st), "memset");
         int32_t* d_list = nullptr;
         if (S.need_list) {
@@ -978,7 +984,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
                 cuda_check(launch_row_kernel(L, S.fast ? kAccLP : S.acc, S.fast ? false : S.flat, S.variant, st),
                            "symbolic L2 kernel");
             } else if (pc.fast) {
-                cuda_check(launch_symbolic_fast(L, S.variant == kVarSymCompressed, d_retry_cnt, d_retry, st),
+                cuda_check(launch_symbolic_fast(L, S.variant == kVarSymCompressed, S.short_rows, d_retry_cnt, d_retry, st),
                            "symbolic kernel");
             } else {
                 cuda_check(launch_row_kernel(L, S.acc, S.flat, S.variant, st), "symbolic kernel");

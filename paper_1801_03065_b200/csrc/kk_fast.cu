@@ -570,7 +570,7 @@ int numeric_flat_fast_blocks_per_sm(int wpb, size_t smem)
 // ---------------------------------------------------------------------------
 // symbolic: order-free union, LP table of {key, word} slots
 // ---------------------------------------------------------------------------
-template <bool kCompressed>
+template <bool kCompressed, bool kPipe>
 __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, unsigned long long* retry_count,
                                                             int32_t* retry_list)
 {
@@ -592,25 +592,13 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
     __syncwarp();
 
     const int64_t nwarps = (int64_t)gridDim.x * L.wpb;
-    const int64_t* __restrict__ a_rowptr = L.a_rowptr;
-    const int32_t* __restrict__ a_cols = L.a_cols;
     const int64_t* __restrict__ b_rowptr = L.b_rowptr;
+    int32_t used = 0; // claimed slots of the current row (warp-uniform)
+    bool overflow = false;
+    bool prev_claimed = false;
 
-    for (int64_t r = (int64_t)blockIdx.x * L.wpb + wib; r < L.nrows; r += nwarps) {
-        const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
-        const int64_t abeg = __ldg(a_rowptr + i), aend = __ldg(a_rowptr + i + 1);
-        int32_t used = 0; // claimed slots (warp-uniform after each window)
-        bool overflow = false;
-        bool prev_claimed = false;
-        for (int64_t p0 = abeg; p0 < aend && !overflow; p0 += 32) {
-            const int na = static_cast<int>(aend - p0 < 32 ? aend - p0 : 32);
-            int64_t bb = 0;
-            int32_t bl = 0;
-            if (lane < na) {
-                const int32_t j = __ldg(a_cols + p0 + lane);
-                bb = __ldg(b_rowptr + j);
-                bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
-            }
+    // one chunk of <= 32 A entries of the current row, B-row descriptors in registers
+    auto chunk = [&](int na, int64_t bb, int32_t bl) {
             // probe / claim / OR one (key, word); true when this lane claimed a slot
             auto insert = [&](int32_t key, uint32_t word) -> bool {
                 bool claimed = false;
@@ -688,7 +676,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                         break;
                     }
                 }
-                continue;
+                return;
             }
             FlatMap<false> fm;
             fm.init(bb, bl, 0.0, lane, scratch);
@@ -718,7 +706,9 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                     break;
                 }
             }
-        }
+    };
+    // size of the finished row (or its hand-off to the L2 path); table reset
+    auto finish = [&](int32_t i) {
         used += __popc(__ballot_sync(kFull, prev_claimed));
         overflow = overflow || used > cap;
         __syncwarp();
@@ -740,6 +730,115 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                 L.sym_sizes[i] = size;
         }
         __syncwarp();
+        used = 0;
+        overflow = false;
+        prev_claimed = false;
+    };
+
+    if constexpr (!kPipe) {
+        // rows with many products: one row at a time
+        for (int64_t r = (int64_t)blockIdx.x * L.wpb + wib; r < L.nrows; r += nwarps) {
+            const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+            const int64_t abeg = __ldg(L.a_rowptr + i), aend = __ldg(L.a_rowptr + i + 1);
+            for (int64_t p0 = abeg; p0 < aend && !overflow; p0 += 32) {
+                const int na = static_cast<int>(aend - p0 < 32 ? aend - p0 : 32);
+                int64_t bb = 0;
+                int32_t bl = 0;
+                if (lane < na) {
+                    const int32_t j = __ldg(L.a_cols + p0 + lane);
+                    bb = __ldg(b_rowptr + j);
+                    bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
+                }
+                chunk(na, bb, bl);
+            }
+            finish(i);
+        }
+        return;
+    }
+    // Short rows: taken 32 at a time and their dependent loads pipelined
+    // across rows (A entries two rows ahead, B-row descriptors one ahead;
+    // three register sets unrolled by three), as in numeric_lp_flat_kernel.
+    for (int64_t r0 = ((int64_t)blockIdx.x * L.wpb + wib) * 32; r0 < L.nrows; r0 += nwarps * 32) {
+        const int nr = static_cast<int>(L.nrows - r0 < 32 ? L.nrows - r0 : 32);
+        int32_t rrow = 0, ralen = 0;
+        int64_t rab = 0;
+        if (lane < nr) {
+            rrow = L.list ? __ldg(L.list + r0 + lane) : static_cast<int32_t>(r0 + lane);
+            rab = __ldg(L.a_rowptr + rrow);
+            ralen = static_cast<int32_t>(__ldg(L.a_rowptr + rrow + 1) - rab);
+        }
+        uint32_t todo = nr == 32 ? kFull : ((1u << nr) - 1u);
+        auto pop = [&]() {
+            const int q = todo ? __ffs(todo) - 1 : -1;
+            todo &= todo - 1;
+            return q;
+        };
+        auto s1 = [&](int q, int32_t& j) {
+            j = 0;
+            if (q < 0)
+                return;
+            const int32_t len = __shfl_sync(kFull, ralen, q);
+            const int64_t ab = __shfl_sync(kFull, rab, q);
+            if (len <= 32 && lane < len)
+                j = __ldg(L.a_cols + ab + lane);
+        };
+        auto s2 = [&](int q, int32_t j, int64_t& bb, int32_t& bl) {
+            bb = 0;
+            bl = 0;
+            if (q < 0)
+                return;
+            const int32_t len = __shfl_sync(kFull, ralen, q);
+            if (len <= 32 && lane < len) {
+                bb = __ldg(b_rowptr + j);
+                bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
+            }
+        };
+        auto s3 = [&](int q, int64_t bb, int32_t bl) {
+            const int32_t len = __shfl_sync(kFull, ralen, q);
+            const int32_t i = __shfl_sync(kFull, rrow, q);
+            if (len <= 32) {
+                chunk(len, bb, bl);
+            } else {
+                const int64_t ab = __shfl_sync(kFull, rab, q);
+                for (int64_t p0 = ab; p0 < ab + len && !overflow; p0 += 32) {
+                    const int na = static_cast<int>(ab + len - p0 < 32 ? ab + len - p0 : 32);
+                    int64_t cbb = 0;
+                    int32_t cbl = 0;
+                    if (lane < na) {
+                        const int32_t jj = __ldg(L.a_cols + p0 + lane);
+                        cbb = __ldg(b_rowptr + jj);
+                        cbl = kCompressed ? __ldg(L.csize + jj) : static_cast<int32_t>(__ldg(b_rowptr + jj + 1) - cbb);
+                    }
+                    chunk(na, cbb, cbl);
+                }
+            }
+            finish(i);
+        };
+        int32_t jA, jB, jC;
+        int64_t bA = 0, bB = 0, bC = 0;
+        int32_t lA = 0, lB = 0, lC = 0;
+        int qA = pop(), qB = pop(), qC = -1;
+        s1(qA, jA);
+        s1(qB, jB);
+        s2(qA, jA, bA, lA);
+        while (qA >= 0) {
+            qC = pop();
+            s1(qC, jC);
+            s2(qB, jB, bB, lB);
+            s3(qA, bA, lA);
+            if (qB < 0)
+                break;
+            qA = pop();
+            s1(qA, jA);
+            s2(qC, jC, bC, lC);
+            s3(qB, bB, lB);
+            if (qC < 0)
+                break;
+            qB = pop();
+            s1(qB, jB);
+            s2(qA, jA, bA, lA);
+            s3(qC, bC, lC);
+        }
     }
 }
 
@@ -779,33 +878,45 @@ int numeric_fast_blocks_per_sm(int wpb, size_t smem)
     return b > 0 ? b : 1;
 }
 
-cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, unsigned long long* retry_count,
+namespace {
+const void* symbolic_flat_fn(bool compressed, bool pipe)
+{
+    return compressed ? (pipe ? reinterpret_cast<const void*>(&symbolic_flat_kernel<true, true>)
+                              : reinterpret_cast<const void*>(&symbolic_flat_kernel<true, false>))
+                      : (pipe ? reinterpret_cast<const void*>(&symbolic_flat_kernel<false, true>)
+                              : reinterpret_cast<const void*>(&symbolic_flat_kernel<false, false>));
+}
+} // namespace
+
+cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, bool pipe, unsigned long long* retry_count,
                                  int32_t* retry_list, cudaStream_t st)
 {
     if (L.nrows <= 0 || L.grid <= 0)
         return cudaSuccess;
     const size_t smem = (size_t)L.wpb * L.lay.bytes;
-    const void* fn = compressed ? reinterpret_cast<const void*>(&symbolic_flat_kernel<true>)
-                                : reinterpret_cast<const void*>(&symbolic_flat_kernel<false>);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(symbolic_flat_fn(compressed, pipe),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess)
             return e;
     }
     RowLaunch Lx = L;
     Lx.no_segments = getenv("KK_SYM_NOSEG") != nullptr;
-    if (compressed)
-        symbolic_flat_kernel<true><<<L.grid, L.wpb * 32, smem, st>>>(Lx, retry_count, retry_list);
+    if (compressed && pipe)
+        symbolic_flat_kernel<true, true><<<L.grid, L.wpb * 32, smem, st>>>(Lx, retry_count, retry_list);
+    else if (compressed)
+        symbolic_flat_kernel<true, false><<<L.grid, L.wpb * 32, smem, st>>>(Lx, retry_count, retry_list);
+    else if (pipe)
+        symbolic_flat_kernel<false, true><<<L.grid, L.wpb * 32, smem, st>>>(Lx, retry_count, retry_list);
     else
-        symbolic_flat_kernel<false><<<L.grid, L.wpb * 32, smem, st>>>(Lx, retry_count, retry_list);
+        symbolic_flat_kernel<false, false><<<L.grid, L.wpb * 32, smem, st>>>(Lx, retry_count, retry_list);
     count_launch();
     return cudaGetLastError();
 }
 
-int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem)
+int symbolic_fast_blocks_per_sm(bool compressed, bool pipe, int wpb, size_t smem)
 {
-    const void* fn = compressed ? reinterpret_cast<const void*>(&symbolic_flat_kernel<true>)
-                                : reinterpret_cast<const void*>(&symbolic_flat_kernel<false>);
+    const void* fn = symbolic_flat_fn(compressed, pipe);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int b = 0;

@@ -113,9 +113,9 @@ cudaError_t launch_numeric_fast(const RowLaunch& L, cudaStream_t st);
 int numeric_fast_blocks_per_sm(int wpb, size_t smem);
 cudaError_t launch_numeric_flat_fast(const RowLaunch& L, cudaStream_t st);
 int numeric_flat_fast_blocks_per_sm(int wpb, size_t smem);
-cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, unsigned long long* retry_count,
+cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, bool pipe, unsigned long long* retry_count,
                                  int32_t* retry_list, cudaStream_t st);
-int symbolic_fast_blocks_per_sm(bool compressed, int wpb, size_t smem);
+int symbolic_fast_blocks_per_sm(bool compressed, bool pipe, int wpb, size_t smem);
 
 // heavy rows (kk_heavy.cu)
 cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st);
