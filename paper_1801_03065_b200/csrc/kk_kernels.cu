@@ -310,7 +310,7 @@ __device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32
 // without another pass).  G lanes per A row.
 // ---------------------------------------------------------------------------
 template <int G>
-__global__ void __launch_bounds__(256) flops_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,
+__global__ void __launch_bounds__(256, 8) flops_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,
                                                     const int32_t* __restrict__ a_cols,
                                                     const int64_t* __restrict__ b_rowptr,
                                                     const int32_t* __restrict__ csize,
