@@ -992,7 +992,26 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         };
         for (const PhaseClass& pc : S.classes)
             sym_launch(pc, S.need_list ? d_list + pc.off : nullptr, S.need_list ? pc.count : m);
-        if (S.optimistic) {
+        if (S.optimistic && heavy_words > 0) {
+            // rows whose optimistic L1 table overflowed: the CTA bitmap kernel,
+            // its row count read on the device (no host round trip)
+            RowLaunch L{};
+            L.a_rowptr = a->row_offsets;
+            L.a_cols = a->col_indices;
+            L.b_rowptr = b->row_offsets;
+            L.b_cols = b->col_indices;
+            L.csize = d_csize;
+            L.cpair = d_cp;
+            L.list = d_retry;
+            L.nrows = m;             // upper bound; the kernel stops at *d_nrows
+            L.d_nrows = d_retry_cnt;
+            L.sym_sizes = h->d_rowptr + 1;
+            L.ctr = h->d_ctr;
+            cuda_check(launch_symbolic_heavy(L, S.variant == kVarSymCompressed, heavy_words, sm_count(), st),
+                       "symbolic heavy kernel (retries)");
+            cudaFreeAsync(d_retry_cnt, st);
+            cudaFreeAsync(d_retry, st);
+        } else if (S.optimistic) {
             // rows whose optimistic L1 table overflowed: exact-size HBM tables
             unsigned long long* hretry = reinterpret_cast<unsigned long long*>(hviews + 5);
             cuda_check(cudaMemcpyAsync(hretry, d_retry_cnt, 8, cudaMemcpyDeviceToHost, st), "retry count");

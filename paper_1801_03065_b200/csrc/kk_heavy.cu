@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L,
         if (atomicOr(&bm[w], word) == 0u)
             atomicOr(&sm[w >> 5], 1u << (w & 31));
     };
-    for (int64_t r = blockIdx.x; r < L.nrows; r += gridDim.x) {
+    const int64_t nrows = L.d_nrows ? static_cast<int64_t>(*L.d_nrows) : L.nrows;
+    for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
         const int64_t abeg = __ldg(L.a_rowptr + i), aend = __ldg(L.a_rowptr + i + 1);
         // chunks of 32 A entries: a chunk with many products is split into

@@ -61,6 +61,7 @@ struct RowLaunch {
     const int32_t* list; // nullptr: rows [0, nrows)
     int64_t nrows;
     int32_t row_lo, row_hi; // numeric: only rows in [row_lo, row_hi) when row_hi > 0
+    const unsigned long long* d_nrows; // symbolic heavy kernel: row count on the device (else nrows)
     const unsigned long long* gate; // numeric fast kernel: exit when gate[0..1] == gate[2..3] (replayed)
     int32_t no_segments;            // symbolic fast kernel: always use 32-product windows (A/B switch)
     // outputs
