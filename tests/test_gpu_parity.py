@@ -631,3 +631,26 @@ def test_multiply_host_shard_uploads_band_only(kk, oracle):
     assert np.array_equal(r.c.row_offsets, ro[lo:hi + 1] - ro[lo])
     assert np.array_equal(r.c.col_indices, cols[ro[lo]:ro[hi]])
     assert np.array_equal(r.c.values.view(np.int64), vals[ro[lo]:ro[hi]].view(np.int64))
+
+
+def test_empty_operands_everywhere(kk):
+    """Zero rows, zero columns and zero nnz through multiply, reuse, row ranges,
+    the host multiply and the transpose."""
+    import torch
+    from paper_1801_03065_b200 import host
+    cases = [((0, 5), (5, 7)), ((4, 0), (0, 3)), ((3, 4), (4, 6))]
+    for (m, n), (n2, k) in cases:
+        a = csr_from_triplets(m, n, [])
+        b = csr_from_triplets(n2, k, [])
+        res = kk.multiply(a, b)
+        c = res.c.to_host()
+        assert c.nnz() == 0 and c.row_offsets.tolist() == [0] * (m + 1)
+        for _ in range(3):
+            kk.numeric(a, b, res.handle)
+        cols = torch.empty(1, dtype=torch.int32, device="cuda")
+        vals = torch.empty(1, dtype=torch.float64, device="cuda")
+        kk.numeric_rows(a, b, res.handle, 0, m, cols, vals)
+        r = host.multiply_host(host.PinnedCsr.from_csr(a), host.PinnedCsr.from_csr(b))
+        assert r.c.nnz() == 0 and r.c.row_offsets.tolist() == [0] * (m + 1)
+        t = kk.transpose(a.to_device()).to_host()
+        assert t.num_rows == n and t.nnz() == 0
