@@ -654,3 +654,29 @@ def test_empty_operands_everywhere(kk):
         assert r.c.nnz() == 0 and r.c.row_offsets.tolist() == [0] * (m + 1)
         t = kk.transpose(a.to_device()).to_host()
         assert t.num_rows == n and t.nnz() == 0
+
+
+def test_special_values_bitwise(kk, oracle):
+    """Inf, NaN, signed zeros, subnormals and near-overflow values: the
+    hashing kernels and the slot replay reproduce the reference's value bits
+    (products through __dmul_rn, first product stored as is / -0.0 + v).
+    NaNs match as NaNs: a NaN generated by the hardware (inf - inf, 0 * inf)
+    has a different bit pattern on x86 (0xfff8...) and on the GPU (0x7fff...)."""
+    rng = np.random.default_rng(97)
+    a = random_csr(rng, 300, 300, 0.09)
+    b = random_csr(rng, 300, 300, 0.09)
+    specials = np.array([np.inf, -np.inf, np.nan, -0.0, 0.0, 5e-324, -2.2e-308, 1.7e308, -1.7e308, 1e-300])
+    for x in (a, b):
+        pick = rng.choice(x.nnz(), x.nnz() // 8, replace=False)
+        x.values[pick] = rng.choice(specials, len(pick))
+    ro = oracle.symbolic_row_offsets(a, b)
+    cols, vals = oracle.numeric(a, b, ro)
+    h = kk.symbolic(a, b)
+    nan = np.isnan(vals)
+    assert nan.any() and np.isinf(vals).any()
+    for p in range(4):  # passes 1-2 hashing, 3-4 replay
+        c = kk.numeric(a, b, h).to_host()
+        assert np.array_equal(c.col_indices, cols)
+        assert np.array_equal(np.isnan(c.values), nan), f"pass {p}: NaN positions"
+        assert np.array_equal(c.values[~nan].view(np.int64), vals[~nan].view(np.int64)), f"pass {p}"
+    assert h.replay_state == 2
