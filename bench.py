@@ -69,9 +69,10 @@ def row_sample(a, every: int):
     return CsrMatrix(len(rows), a.num_cols, ro, a.col_indices[idx], a.values[idx], True)
 
 
-def cpu_reference_rate(a, budget_s: float = 12.0, min_every: int = 4):
-    """Time the reference's own multiply (oracle/_ref) on a row sample of the
-    workload with all host threads.  Returns (gflops, cores, kind, sample)."""
+def cpu_reference_sampler(a, budget_s: float = 12.0, min_every: int = 4):
+    """Size a row sample of the workload so one reference multiply (oracle/_ref,
+    all host threads) takes about budget_s/3.  Returns (run, flops, cores, kind,
+    every): run() times one NoReuse multiply of the sample in seconds."""
     cores = os.cpu_count() or 1
     from oracle.oracle import Oracle, Reference, reference_available
     o = Oracle()
@@ -79,34 +80,35 @@ def cpu_reference_rate(a, budget_s: float = 12.0, min_every: int = 4):
         ref, kind = Reference(), "reference"
     else:
         ref, kind = None, "port"
-    # size the sample so one multiply takes ~budget/3
+
+    def run_on(s):
+        if ref is not None:
+            ms, _ = ref.multiply_ms(s, a, worker_count=cores)
+            return ms / 1e3
+        t0 = time.perf_counter()
+        o.multiply(s, a)
+        return time.perf_counter() - t0
+
     every = 256
     while True:
         s = row_sample(a, every)
         _, fl, _ = o.flops_stats(s, a)
-        t0 = time.perf_counter()
-        if ref is not None:
-            ms, _ = ref.multiply_ms(s, a, worker_count=cores)
-            t = ms / 1e3
-        else:
-            o.multiply(s, a)
-            t = time.perf_counter() - t0
+        t = run_on(s)
         if t > budget_s / 3 or every <= min_every:
             break
         every = max(min_every, every // 4)
-    times = [t]
-    for _ in range(2):
-        if ref is not None:
-            ms, _ = ref.multiply_ms(s, a, worker_count=cores)
-            times.append(ms / 1e3)
-        else:
-            t0 = time.perf_counter()
-            o.multiply(s, a)
-            times.append(time.perf_counter() - t0)
+    return (lambda: run_on(s)), fl, (cores if ref else 1), kind, every, s.num_rows
+
+
+def cpu_reference_rate(a, budget_s: float = 12.0, min_every: int = 4):
+    """The reference's multiply on a row sample: mean of three timed runs.
+    Returns (gflops, cores, kind, sample)."""
+    run, fl, cores, kind, every, rows = cpu_reference_sampler(a, budget_s, min_every)
+    times = [run() for _ in range(3)]
     tm = statistics.mean(times)
-    sample = (f"rows 0::{every} of A ({s.num_rows} rows, {fl} mults) times full B; mean of "
-              f"{len(times)} NoReuse multiplies, worker_count={cores if ref else 1}")
-    return 2.0 * fl / tm / 1e9, (cores if ref else 1), kind, sample
+    sample = (f"rows 0::{every} of A ({rows} rows, {fl} mults) times full B; mean of "
+              f"{len(times)} NoReuse multiplies, worker_count={cores}")
+    return 2.0 * fl / tm / 1e9, cores, kind, sample
 
 
 class Clocks:
@@ -185,10 +187,14 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        rate, cores, kind, sample = cpu_reference_rate(a_host)
-        steps = []
-        for _ in range(args.warmup + args.steps):
-            steps.append(rate)
+        # each step: one NoReuse multiply of a row sample sized to ~4 s
+        run, sfl, cores, kind, every, rows = cpu_reference_sampler(a_host)
+        for _ in range(args.warmup):
+            run()
+        times = [run() for _ in range(args.steps)]
+        rate = 2.0 * sfl * len(times) / sum(times) / 1e9
+        sample = (f"rows 0::{every} of A ({rows} rows, {sfl} mults) times full B per step; "
+                  f"{args.steps} timed + {args.warmup} warm-up NoReuse multiplies, worker_count={cores}")
         from oracle.oracle import Oracle
         _, fl, _ = Oracle().flops_stats(a_host, a_host)
         line = {"metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
