@@ -246,11 +246,13 @@ def main():
     cols = torch.empty(max(nnz_c_local, 1), dtype=torch.int32, device=dev)
     vals = torch.empty(max(nnz_c_local, 1), dtype=torch.float64, device=dev)
 
-    def bcast_b():
-        # B broadcast over NCCL from rank 0 every step (the "with broadcast" timing)
+    def bcast_b(values_only: bool = False):
+        # B broadcast over NCCL from rank 0 every step (the "with broadcast"
+        # timing); numeric-only passes re-send only B's values (SURVEY §8e:
+        # the structure is unchanged under reuse)
         if world > 1 and args.broadcast:
-            for t in (B.row_offsets, B.col_indices, B.values):  # in place: ranks > 0 compute on it
-                dist.broadcast(t, src=0)
+            for t in ((B.values,) if values_only else (B.row_offsets, B.col_indices, B.values)):
+                dist.broadcast(t, src=0)  # in place: ranks > 0 compute on it
 
     def step_symnum():
         bcast_b()
@@ -294,7 +296,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            bcast_b()
+            bcast_b(values_only=True)
             kk.numeric(A_shard, B, h, out=(cols, vals))
         e1.record(stream)
         barrier()
