@@ -255,10 +255,11 @@ def main():
                 dist.broadcast(t, src=0)  # in place: ranks > 0 compute on it
 
     def step_symnum():
+        # the reference's multiply: flops/gate, compression, symbolic, scan,
+        # C allocation (torch's caching allocator) and numeric
         bcast_b()
         h = kk.symbolic(A_shard, B)
-        kk.numeric(A_shard, B, h, out=(cols, vals))
-        return h
+        return kk.numeric(A_shard, B, h)
 
     def barrier():
         if world > 1:
