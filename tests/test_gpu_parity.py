@@ -680,3 +680,58 @@ def test_special_values_bitwise(kk, oracle):
         assert np.array_equal(np.isnan(c.values), nan), f"pass {p}: NaN positions"
         assert np.array_equal(c.values[~nan].view(np.int64), vals[~nan].view(np.int64)), f"pass {p}"
     assert h.replay_state == 2
+
+
+def _row_sample(kk, a, rows):
+    lo, hi = a.row_offsets[rows], a.row_offsets[rows + 1]
+    sro = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(hi - lo, out=sro[1:])
+    idx = np.concatenate([np.arange(l, e) for l, e in zip(lo, hi)])
+    return kk.CsrMatrix(len(rows), a.num_cols, sro, a.col_indices[idx], a.values[idx], True)
+
+
+def _check_rows(oracle, a_s, b, ro, cols, vals, rows):
+    oro, ocols, ovals = oracle.multiply(a_s, b)
+    for q, i in enumerate(rows):
+        g0, g1 = int(ro[i]), int(ro[i + 1])
+        assert g1 - g0 == oro[q + 1] - oro[q]
+        assert np.array_equal(cols[g0:g1], ocols[oro[q]:oro[q + 1]])
+        assert np.array_equal(vals[g0:g1].view(np.int64), ovals[oro[q]:oro[q + 1]].view(np.int64))
+
+
+def test_c2_full_size_row_sampled(kk, oracle):
+    """Config 2 at full size (160^3, 2.9 G products): closed-form nnz, and every
+    97th row plus the boundary rows bit-exact against the oracle."""
+    from paper_1801_03065_b200 import generators as G
+    a = G.laplace3d(160)
+    res = kk.multiply(a, a)
+    h = res.handle
+    assert h.nnz_c() == 794 ** 3 and h.flops.total_flops == 1430 ** 3
+    ro = h.c_row_offsets
+    rows = np.unique(np.concatenate([np.arange(0, a.num_rows, 97), np.arange(0, 200),
+                                     np.arange(a.num_rows - 200, a.num_rows)]))
+    _check_rows(oracle, _row_sample(kk, a, rows), a, ro, res.c.col_indices.cpu().numpy(),
+                res.c.values.cpu().numpy(), rows)
+
+
+def test_c5_reuse_passes_row_sampled(kk, oracle):
+    """Config 5 (200^3, one symbolic then numeric passes with perturbed values,
+    SURVEY §8c): passes 1 (hashing) and 3 (slot replay) row-sampled bit-exact."""
+    import torch
+    from paper_1801_03065_b200 import generators as G
+    a = G.laplace3d(200)
+    da = a.to_device()
+    h = kk.symbolic(da, da)
+    assert h.nnz_c() == 994 ** 3
+    ro = h.c_row_offsets
+    rows = np.unique(np.concatenate([np.arange(0, a.num_rows, 211), np.arange(0, 100)]))
+    rng = np.random.default_rng(5)
+    base = a.values.copy()
+    for p in range(3):
+        a.values[:] = base * (1.0 + 1e-3 * rng.uniform(-1.0, 1.0, base.shape))
+        da.values.copy_(torch.from_numpy(a.values))
+        c = kk.numeric(da, da, h)
+        if p in (0, 2):
+            _check_rows(oracle, _row_sample(kk, a, rows), a, ro, c.col_indices.cpu().numpy(),
+                        c.values.cpu().numpy(), rows)
+    assert h.replay_state == 2
