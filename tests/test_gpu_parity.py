@@ -735,3 +735,21 @@ def test_c5_reuse_passes_row_sampled(kk, oracle):
             _check_rows(oracle, _row_sample(kk, a, rows), a, ro, c.col_indices.cpu().numpy(),
                         c.values.cpu().numpy(), rows)
     assert h.replay_state == 2
+
+
+def test_c3_full_size_vs_oracle(kk, oracle):
+    """Config 3 at full size: A (128^3 27-point) * P (2x2x2 aggregation), then
+    R * (AP) with R = P^T built on the device; both products bit-exact vs the
+    oracle, SURVEY §8d counts."""
+    from paper_1801_03065_b200 import generators as G
+    a, p = G.laplace3d(128), G.aggregation(128)
+    dA, dP = a.to_device(), p.to_device()
+    dR = kk.transpose(dP)
+    ap = kk.multiply(dA, dP)
+    assert ap.handle.flops.total_flops == 55_742_968 and ap.handle.nnz_c() == 16_387_064
+    ap_host = ap.c.to_host()
+    assert_parity(oracle, a, p, ap_host)
+    rap = kk.multiply(dR, ap.c)
+    assert rap.handle.flops.total_flops == 16_387_064 and rap.handle.nnz_c() == 6_859_000
+    r = dR.to_host()
+    assert_parity(oracle, r, ap_host, rap.c.to_host())
