@@ -14,7 +14,10 @@
 //
 // numeric_lp_flat_kernel  Thread-Flat-Parallel numeric for short B rows: 32-product
 //     windows, duplicate keys grouped with __match_any_sync and folded by the
-//     lowest lane in lane (= product) order onto the running sum.
+//     lowest lane in lane (= product) order onto the running sum.  Rows are
+//     short and latency-bound, so a warp takes 32 rows at a time and
+//     pipelines their dependent loads across rows (A entries two rows ahead,
+//     B-row descriptors one row ahead).
 //
 // symbolic_flat_kernel    Thread-Flat-Parallel structure union (engine.cpp:268-286
 //     with SymbolicSink :210-221) over the compressed graph (or raw columns).
@@ -22,7 +25,14 @@
 //     window are resolved with shared-memory CAS/OR instead of a warp fold,
 //     and the row size is the popcount of the table (no position bookkeeping).
 //     Tables are sized optimistically from the row bound; a row that overflows
-//     its table is re-queued to the HBM (L2) path, which is sized exactly.
+//     its table is re-queued to the exact-size path.  Chunks of very short
+//     compressed rows run as segmented steps (several whole B rows per 32
+//     lanes); plans of short rows use the same row pipeline as the flat
+//     numeric kernel.
+//
+// The flattened-window map (FlatMap) compacts a chunk's non-empty segments
+// through shared memory and locates each lane's segment from a bitmask of
+// segment starts (REDUX.OR + popc) instead of a per-window binary search.
 #include <cstdint>
 #include <cstdlib>
 
