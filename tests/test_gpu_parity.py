@@ -753,3 +753,16 @@ def test_c3_full_size_vs_oracle(kk, oracle):
     assert rap.handle.flops.total_flops == 16_387_064 and rap.handle.nnz_c() == 6_859_000
     r = dR.to_host()
     assert_parity(oracle, r, ap_host, rap.c.to_host())
+
+
+def test_fuzz_short():
+    """scripts/fuzz.py for 20 s (random shapes, configs and paths vs the oracle;
+    the round-1 log has 60,630 cases over two 10-minute runs)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz.py"), "20", "7"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "fuzz ok" in r.stdout
