@@ -757,7 +757,7 @@ def test_c3_full_size_vs_oracle(kk, oracle):
 
 def test_fuzz_short():
     """scripts/fuzz.py for 20 s (random shapes, configs and paths vs the oracle;
-    the round-1 log has 60,630 cases over two 10-minute runs)."""
+    the round-1 log has 87,973 cases over three runs, profiles/r01_fuzz.md)."""
     import os
     import subprocess
     import sys
