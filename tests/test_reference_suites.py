@@ -30,6 +30,13 @@ def _bin(name):
 
 
 def _run(path, timeout):
+    try:  # hand device memory cached by earlier tests in this process back
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+    except Exception:
+        pass
     r = subprocess.run([path], capture_output=True, text=True, timeout=timeout, cwd=REF)
     return r.returncode, r.stdout + r.stderr
 
