@@ -5,8 +5,10 @@
                  compiled from /root/reference/proj/src (present when it was
                  built in this container; the built .so travels to the GPU box).
 
-Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
-``--impl reference`` legs may import this module, and only as the checker.
+Only tests/ (incl. tests/tools/), __graft_entry__.smoke() and the CPU-baseline
+legs of bench.py (cpu_baseline, ``--impl reference``) and of its companion for
+the other BASELINE configs, scripts/bench_configs.py, may import this module,
+and only as the checker or the timed reference.
 """
 from __future__ import annotations
 

@@ -756,13 +756,13 @@ def test_c3_full_size_vs_oracle(kk, oracle):
 
 
 def test_fuzz_short():
-    """scripts/fuzz.py for 20 s (random shapes, configs and paths vs the oracle;
+    """tests/tools/fuzz.py for 20 s (random shapes, configs and paths vs the oracle;
     the round-1 log has 87,973 cases over three runs, profiles/r01_fuzz.md)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz.py"), "20", "7"],
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "tools", "fuzz.py"), "20", "7"],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "fuzz ok" in r.stdout

@@ -1,6 +1,6 @@
 """Debug helper: which (phase, accumulator, scheme, compression) disagrees with the oracle."""
 import sys, os, numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))  # repo root
 import paper_1801_03065_b200 as kk
 from paper_1801_03065_b200 import generators as G
 from oracle.oracle import Oracle

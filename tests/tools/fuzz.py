@@ -6,14 +6,16 @@ Each case draws shapes, densities, row-length skew, sortedness, a config
 multiply) and checks C against the C oracle bit for bit (raw order when
 the reference's raw order is defined, sorted otherwise).
 
-    python scripts/fuzz.py [seconds] [seed]
+    python tests/tools/fuzz.py [seconds] [seed]
+
+Test infrastructure: the oracle is the checker.
 """
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))  # repo root
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # tests/ (conftest helpers)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 

@@ -1,7 +1,7 @@
 """Config 4 (R-MAT scale 20, ef 16) end to end on one GPU: symbolic stats vs
 SURVEY §8d, numeric timing, row-sampled parity vs the oracle."""
 import sys, os, time, json
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))  # repo root
 import numpy as np, torch
 import paper_1801_03065_b200 as kk
 from paper_1801_03065_b200 import generators as G
