@@ -442,14 +442,27 @@ void free_pool(DevPool& pool)
     pool = DevPool{};
 }
 
+// Per-thread pinned scratch for the symbolic phase's small host reads.
+// Pinned allocation and release synchronise the whole device (they would wait
+// for unrelated copies on other streams, e.g. an overlapped upload), so the
+// buffer is allocated once per thread and kept.
 struct PinnedBuf {
     void* p = nullptr;
     explicit PinnedBuf(size_t n)
     {
-        if (cudaMallocHost(&p, n) != cudaSuccess)
-            fail(SPG_ERR_NOMEM, "pinned host buffer");
+        thread_local void* buf = nullptr;
+        thread_local size_t cap = 0;
+        if (cap < n) {
+            if (buf)
+                cudaFreeHost(buf);
+            buf = nullptr;
+            cap = 0;
+            if (cudaMallocHost(&buf, n) != cudaSuccess)
+                fail(SPG_ERR_NOMEM, "pinned host buffer");
+            cap = n;
+        }
+        p = buf;
     }
-    ~PinnedBuf() { cudaFreeHost(p); }
 };
 
 void validate_csr(const spg_csr* x, const char* name, bool need_vals)
