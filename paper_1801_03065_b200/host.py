@@ -9,7 +9,8 @@ around the copies:
 
   * the operands' structure (row offsets, columns) is uploaded first and their
     values on a second stream, overlapping the symbolic phase (which reads
-    structure only);
+    structure only); for C = A*A the values go in row chunks and each block
+    of C waits only for the chunks up to the last row it references;
   * a matrix passed as both A and B (C = A*A) is uploaded once; `a_rows`
     names A as a row block of B (the row-sharded multi-GPU case) so only B
     travels, and only B's row offsets plus the rows in the block's column band
@@ -137,11 +138,27 @@ def multiply_host(a: PinnedCsr, b: Optional[PinnedCsr] = None, cfg: Optional[Spg
             r0 = min(lo, int(acols.min()))
             r1 = max(hi, int(acols.max()) + 1)
             band = (r0, r1)
+    chunk_rows, chunk_events = [], []  # B's values in row chunks (C = A*A path)
     if band is None:
         ro_b, ci_b = up_structure(src_b)
         side.wait_stream(main)
-        with torch.cuda.stream(side):
-            v_b = src_b.values.to(dev, non_blocking=True)
+        if same and src_b.nnz() >= (1 << 22):
+            # values in 8 row chunks, each with an event: a block of C waits
+            # only for the B rows it references
+            v_b = torch.empty(max(src_b.nnz(), 1), dtype=torch.float64, device=dev)
+            bc = _row_cuts(b_ro_host, 0, src_b.num_rows, 8)
+            with torch.cuda.stream(side):
+                for c0, c1 in zip(bc[:-1], bc[1:]):
+                    q0, q1 = int(b_ro_host[c0]), int(b_ro_host[c1])
+                    if q1 > q0:
+                        v_b[q0:q1].copy_(src_b.values[q0:q1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    chunk_rows.append(c1)
+                    chunk_events.append(ev)
+        else:
+            with torch.cuda.stream(side):
+                v_b = src_b.values.to(dev, non_blocking=True)
         h2d = src_b.nbytes()
     else:
         # full row offsets; columns/values of the band rows at their own offsets
@@ -174,6 +191,15 @@ def multiply_host(a: PinnedCsr, b: Optional[PinnedCsr] = None, cfg: Optional[Spg
     if blocks is None:
         blocks = 1 if nnz_a < (1 << 22) else 8
     cuts = _row_cuts(a_host_ro, lo, hi, blocks)
+    # the last B row each block of A references (its own rows included): the
+    # value chunk it waits for
+    need_row = None
+    if chunk_events:
+        tops = []
+        for r0, r1 in zip(cuts[:-1], cuts[1:]):
+            q0, q1 = int(a_host_ro[r0]), int(a_host_ro[r1])
+            tops.append(ci_b[q0:q1].max() if q1 > q0 else torch.zeros((), dtype=torch.int32, device=dev))
+        need_row = [max(int(t), r1 - 1) for t, r1 in zip(torch.stack(tops).cpu().tolist(), cuts[1:])]
 
     # ---- one symbolic over A's structure (overlaps the value upload) ----
     dA = dA_full.row_block(lo, hi)
@@ -196,8 +222,12 @@ def multiply_host(a: PinnedCsr, b: Optional[PinnedCsr] = None, cfg: Optional[Spg
         o_ro[:m + 1].copy_(c_ro, non_blocking=True)
 
     # ---- numeric per row block; block k's C copies out while block k+1 computes ----
-    main.wait_event(values_ready)
-    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+    if need_row is None:
+        main.wait_event(values_ready)
+    for k, (r0, r1) in enumerate(zip(cuts[:-1], cuts[1:])):
+        if need_row is not None:
+            c = next(q for q, e in enumerate(chunk_rows) if e > need_row[k])
+            main.wait_event(chunk_events[c])
         b0, b1 = r0 - lo, r1 - lo
         numeric_rows(dA, dB, h, b0, b1, d_ci, d_v, stream=main)
         done = torch.cuda.Event()
