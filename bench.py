@@ -354,7 +354,7 @@ def main():
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
-        ksteps = max(1, min(args.steps, 3))
+        ksteps = max(1, min(args.steps, 5))
         t0.record(stream)
         for _ in range(ksteps):
             r = e2e_step()
