@@ -18,9 +18,11 @@
  * which is how multi-GPU shards are passed.
  *
  * Calls are stream-ordered on `stream` (a cudaStream_t, NULL = legacy default
- * stream).  spg_symbolic synchronises the stream (it needs two small host
- * reads to take the reference's host-side decisions); spg_numeric is fully
- * asynchronous unless `stats` is non-NULL.
+ * stream).  spg_symbolic synchronises the stream (small host reads for the
+ * reference's host-side decisions: flop/compression totals, nnz(C));
+ * spg_numeric is asynchronous unless `stats` is non-NULL, except for the one
+ * pass per handle that records the structure-reuse slot replay.  One handle
+ * must not run concurrent spg_numeric calls.
  */
 #ifndef KKSPGEMM_H
 #define KKSPGEMM_H
