@@ -757,7 +757,7 @@ def test_c3_full_size_vs_oracle(kk, oracle):
 
 def test_fuzz_short():
     """tests/tools/fuzz.py for 20 s (random shapes, configs and paths vs the oracle;
-    the round-1 log has 109,542 cases over four runs, profiles/r01_fuzz.md)."""
+    the round-1 log has 141,544 cases over five runs, profiles/r01_fuzz.md)."""
     import os
     import subprocess
     import sys
