@@ -5,6 +5,8 @@
 // touches matrix data runs in the kernels of kk_kernels.cu.
 #include <algorithm>
 #include <cmath>
+#include <climits>
+#include <cstddef>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -122,6 +124,38 @@ template <class T> T* dalloc(size_t count, cudaStream_t st, const char* what)
     void* p = nullptr;
     cuda_check(cudaMallocAsync(&p, std::max<size_t>(count * sizeof(T), 16), st), what);
     return static_cast<T*>(p);
+}
+
+// Key capacity of the reference's level-1 accumulator for a resolved choice:
+// LlAccumulator holds l1_capacity keys (accumulators.hpp:63-151), the owning
+// LpAccumulator max_new = min(ceil(occ * cap), cap - 1) with cap =
+// ceil_pow2(ceil(l1 / occ)) (accumulators.hpp:158-190), Dense is single-level.
+// Used only for the reference's PhaseStats (pool_allocations, l2_inserts).
+int32_t ref_l1_keys(const spg_resolved& rc, double occ)
+{
+    const int64_t l1 = std::max<int64_t>(rc.l1_capacity, 1);
+    if (rc.accumulator == SPG_ACC_LL)
+        return static_cast<int32_t>(l1);
+    if (rc.accumulator == SPG_ACC_LP) {
+        const double o = std::max(occ, 1e-6);
+        const int64_t cap = ceil_pow2_i(static_cast<int64_t>(std::ceil(static_cast<double>(l1) / o)));
+        return static_cast<int32_t>(std::min<int64_t>(static_cast<int64_t>(std::ceil(occ * cap)), cap - 1));
+    }
+    return INT32_MAX;
+}
+
+// plan_pool's PoolSizingError (memory_pool.cpp:97-99): the reference sizes a
+// pool for every LL/LP phase, one chunk = l2_capacity slots rounded to a
+// 64-byte line (32 bytes per slot); a chunk above the budget is an error even
+// when no row would spill.
+void check_pool_budget(const spg_resolved& rc, int64_t budget)
+{
+    if (rc.accumulator != SPG_ACC_LL && rc.accumulator != SPG_ACC_LP)
+        return;
+    const int64_t bound = std::max<int64_t>(rc.l2_capacity, 1);
+    const int64_t chunk = (bound + 1) / 2 * 2 * 32;
+    if (chunk > budget)
+        fail(SPG_ERR_POOL_SIZING, "plan_pool: a single chunk exceeds the memory budget");
 }
 
 } // namespace
@@ -271,16 +305,15 @@ L2Spec plan_l2(int acc, int variant, int64_t s_true, int32_t domain, int64_t row
     if (static_cast<int64_t>(S.chunk_bytes) > cfg.pool_budget_bytes)
         fail(SPG_ERR_POOL_SIZING, "plan_pool: a single chunk exceeds the memory budget");
     const int64_t workers = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sm_count() * 16));
-    const int64_t by_budget = cfg.pool_budget_bytes / static_cast<int64_t>(S.chunk_bytes);
     // memory_pool.cpp:83-109: one chunk per worker (one2one) or 2x (many2many),
-    // halved under the budget, falling back to many2many below the worker count
+    // halved while over the budget, falling back to many2many below the
+    // worker count
     int64_t chunks = cfg.pool_mode == SPG_POOL_ONE2ONE ? workers : 2 * workers;
     S.pool_mode = cfg.pool_mode == SPG_POOL_ONE2ONE ? 0 : 1;
-    if (chunks > by_budget) {
-        chunks = std::max<int64_t>(1, by_budget);
-        if (chunks < workers)
-            S.pool_mode = 1;
-    }
+    while (chunks * static_cast<int64_t>(S.chunk_bytes) > cfg.pool_budget_bytes && chunks > 1)
+        chunks = std::max<int64_t>(1, chunks / 2);
+    if (chunks < workers)
+        S.pool_mode = 1;
     S.num_chunks = static_cast<int32_t>(chunks);
     S.wpb = 8;
     const int64_t warps = S.pool_mode == 0 ? chunks : workers;
@@ -445,23 +478,45 @@ void free_pool(DevPool& pool)
 // Per-thread pinned scratch for the symbolic phase's small host reads.
 // Pinned allocation and release synchronise the whole device (they would wait
 // for unrelated copies on other streams, e.g. an overlapped upload), so the
-// buffer is allocated once per thread and kept.
+// buffer is allocated once per thread and kept; it is portable (valid in every
+// context), freed when the thread exits, and re-allocated if the runtime no
+// longer recognises it (e.g. after a device reset).  spg_symbolic synchronises
+// its stream before returning on every path, so no copy into the buffer is
+// still in flight when the next call reuses it.
+struct PinnedCache {
+    void* buf = nullptr;
+    size_t cap = 0;
+    ~PinnedCache()
+    {
+        if (buf)
+            cudaFreeHost(buf); // may fail harmlessly at process teardown
+    }
+    bool valid() const
+    {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, buf) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return at.type == cudaMemoryTypeHost;
+    }
+};
+
 struct PinnedBuf {
     void* p = nullptr;
     explicit PinnedBuf(size_t n)
     {
-        thread_local void* buf = nullptr;
-        thread_local size_t cap = 0;
-        if (cap < n) {
-            if (buf)
-                cudaFreeHost(buf);
-            buf = nullptr;
-            cap = 0;
-            if (cudaMallocHost(&buf, n) != cudaSuccess)
+        thread_local PinnedCache c;
+        if (c.cap < n || (c.buf && !c.valid())) {
+            if (c.buf && c.valid())
+                cudaFreeHost(c.buf);
+            c.buf = nullptr;
+            c.cap = 0;
+            if (cudaHostAlloc(&c.buf, n, cudaHostAllocPortable) != cudaSuccess)
                 fail(SPG_ERR_NOMEM, "pinned host buffer");
-            cap = n;
+            c.cap = n;
         }
-        p = buf;
+        p = c.buf;
     }
 };
 
@@ -505,6 +560,8 @@ struct spg_handle {
     bool numeric_forced = false;
     PhasePlan num;
     int32_t* d_num_list = nullptr;
+    int32_t* d_empty_list = nullptr; // rows of C the structure leaves empty (checked every pass)
+    int64_t n_empty = 0;
     DevPool num_pool;
     cudaStream_t stream = nullptr;
     // heavy numeric rows (kk_heavy.cu): per-CTA staging for the bucket scatter
@@ -556,6 +613,8 @@ struct spg_handle {
             cudaFree(d_ctr);
         if (d_num_list)
             cudaFree(d_num_list);
+        if (d_empty_list)
+            cudaFree(d_empty_list);
         free_pool(num_pool);
     }
 };
@@ -610,6 +669,18 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
     if (h->d_num_list) {
         cudaFreeAsync(h->d_num_list, st);
         h->d_num_list = nullptr;
+    }
+    if (h->d_empty_list) {
+        cudaFreeAsync(h->d_empty_list, st);
+        h->d_empty_list = nullptr;
+    }
+    h->n_empty = static_cast<int64_t>(h->size_hist.hist[0]);
+    if (h->n_empty > 0) {
+        h->d_empty_list = dalloc<int32_t>(h->n_empty, st, "empty row list");
+        auto* cnt = dalloc<unsigned long long>(1, st, "count");
+        cuda_check(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st), "memset");
+        cuda_check(launch_collect_empty_rows(h->info.m, h->d_rowptr, h->d_empty_list, cnt, st), "empty rows");
+        cudaFreeAsync(cnt, st);
     }
     if (h->num_heavy)
         h->num.need_list = true; // heavy rows are queued largest first
@@ -931,6 +1002,8 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
                        ? cudaSuccess
                        : cudaErrorInvalidValue,
                    "resolve_config");
+        check_pool_budget(I.symbolic_choice, cfg.pool_budget_bytes);
+        const int32_t sym_l1_keys = ref_l1_keys(I.symbolic_choice, cfg.lp_max_occupancy);
 
         // ---- K5: symbolic union ----
         const int variant = apply ? kVarSymCompressed : kVarSymRaw;
@@ -982,6 +1055,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             L.nrows = nrows;
             L.sym_sizes = h->d_rowptr + 1;
             L.ctr = h->d_ctr;
+            L.l1_keys = sym_l1_keys;
             L.lay = pc.lay;
             L.wpb = pc.wpb;
             L.grid = pc.grid;
@@ -1020,6 +1094,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             L.d_nrows = d_retry_cnt;
             L.sym_sizes = h->d_rowptr + 1;
             L.ctr = h->d_ctr;
+            L.l1_keys = sym_l1_keys;
             cuda_check(launch_symbolic_heavy(L, S.variant == kVarSymCompressed, heavy_words, sm_count(), st),
                        "symbolic heavy kernel (retries)");
             cudaFreeAsync(d_retry_cnt, st);
@@ -1078,6 +1153,9 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         *out = h;
     });
     if (rc != SPG_OK) {
+        // copies into the per-thread pinned scratch may still be in flight
+        cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+        cudaGetLastError();
         delete h;
         if (out)
             *out = nullptr;
@@ -1103,6 +1181,8 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
         if (row_lo < 0 || row_hi > I.m || row_lo > row_hi)
             fail(SPG_ERR_CONTRACT, "numeric: bad row range");
         const bool full = row_lo == 0 && row_hi == I.m;
+        check_pool_budget(I.numeric_choice, I.config.pool_budget_bytes); // raised by numeric (run_phase)
+        const int32_t num_l1_keys = ref_l1_keys(I.numeric_choice, I.config.lp_max_occupancy);
         require_device();
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         h->stream = st;
@@ -1112,7 +1192,16 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
             cuda_check(cudaEventCreate(&e1), "event");
             cuda_check(cudaEventRecord(e0, st), "event");
         }
-        cuda_check(cudaMemsetAsync(h->d_ctr, 0, sizeof(DevCounters), st), "memset");
+        // per-call counters and queue heads restart every call; the error word
+        // restarts only with a pass that begins at row 0, so a caller running
+        // a pass as row blocks (host.multiply_host) sees an error raised by
+        // any block when it checks after the last one
+        if (row_lo == 0) {
+            cuda_check(cudaMemsetAsync(h->d_ctr, 0, sizeof(DevCounters), st), "memset");
+        } else {
+            cuda_check(cudaMemsetAsync(h->d_ctr, 0, offsetof(DevCounters, error), st), "memset");
+            cuda_check(cudaMemsetAsync(&h->d_ctr->next_row, 0, sizeof(h->d_ctr->next_row), st), "memset");
+        }
         const PhasePlan& P = h->num;
         if (full)
             ++h->numeric_calls;
@@ -1131,6 +1220,10 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
                        "replay numeric");
             replayed = true;
         }
+        if (h->n_empty > 0 && row_hi > row_lo)
+            cuda_check(launch_check_empty_rows(h->d_empty_list, h->n_empty, a->row_offsets, a->col_indices,
+                                               b->row_offsets, full ? 0 : row_lo, full ? 0 : row_hi, h->d_ctr, st),
+                       "empty rows check");
         if (!replayed && P.l2_class >= 0 && !h->num_heavy)
             ensure_pool(h->num_pool, P.l2, st);
         for (const PhaseClass& pc : P.classes) {
@@ -1152,6 +1245,7 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
             L.c_cols = c_cols;
             L.c_vals = c_vals;
             L.ctr = h->d_ctr;
+            L.l1_keys = num_l1_keys;
             L.lay = pc.lay;
             L.wpb = pc.wpb;
             L.grid = pc.grid;

@@ -207,10 +207,15 @@ template <> __device__ __forceinline__ uint32_t combine<uint32_t>(uint32_t a, ui
 // One work item: every lane holds at most one (key, payload) product.
 // Returns nothing; advances the warp-uniform first-touch counter `cnt`.
 // kCountOnly: payload is the constant 1 (raw symbolic) and is not stored.
+// spill counts the products whose key's first-touch rank is >= l1_keys: the
+// products the reference's two-level accumulators send to level 2
+// (engine.cpp:78-87 — a key outside the first l1_keys distinct keys of the row
+// finds L1 full), i.e. PhaseStats::l2_inserts.
 template <bool kFlat, bool kCountOnly, class Map, class P>
 __device__ __forceinline__ void accumulate_item(bool valid, int32_t key, P v, Map& map,
                                                 int32_t* ids, P* pay, int32_t cap,
-                                                int32_t& cnt, DevCounters* ctr, int lane)
+                                                int32_t& cnt, DevCounters* ctr, int lane,
+                                                int32_t l1_keys, int64_t& spill)
 {
     bool active = valid;
     uint32_t rest = 0;
@@ -241,6 +246,8 @@ __device__ __forceinline__ void accumulate_item(bool valid, int32_t key, P v, Ma
         }
     }
     cnt += __popc(nm);
+    if (ok && pos >= l1_keys)
+        spill += 1 + __popc(rest);
     if constexpr (kCountOnly) {
         __syncwarp();
         return;
@@ -274,7 +281,7 @@ __device__ __forceinline__ int32_t warp_row(const int64_t* __restrict__ a_rowptr
                                             const double* __restrict__ a_vals, int32_t i,
                                             const Src& src, Map& map, int32_t* ids, P* pay,
                                             int32_t cap, DevCounters* ctr, int lane,
-                                            int64_t& products)
+                                            int32_t l1_keys, int64_t& spill)
 {
     constexpr bool kNumeric = std::is_same<P, double>::value;
     const int64_t abeg = __ldg(a_rowptr + i);
@@ -296,7 +303,6 @@ __device__ __forceinline__ int32_t warp_row(const int64_t* __restrict__ a_rowptr
                 const int64_t base = __shfl_sync(kFull, bbase, q);
                 const int64_t len = __shfl_sync(kFull, blen, q);
                 const double a = __shfl_sync(kFull, av, q);
-                products += len;
                 for (int64_t t0 = 0; t0 < len; t0 += 32) {
                     const int64_t t = t0 + lane;
                     const bool valid = t < len;
@@ -308,7 +314,7 @@ __device__ __forceinline__ int32_t warp_row(const int64_t* __restrict__ a_rowptr
                             v = src.payload(base + t, a);
                     }
                     accumulate_item<false, kCountOnly>(valid, key, v, map, ids, pay, cap, cnt,
-                                                       ctr, lane);
+                                                       ctr, lane, l1_keys, spill);
                 }
             }
         } else {
@@ -321,7 +327,6 @@ __device__ __forceinline__ int32_t warp_row(const int64_t* __restrict__ a_rowptr
             }
             const int64_t excl = incl - blen;
             const int64_t total = __shfl_sync(kFull, incl, 31);
-            products += total;
             for (int64_t w0 = 0; w0 < total; w0 += 32) {
                 const int64_t t = w0 + lane;
                 const bool valid = t < total;
@@ -344,7 +349,7 @@ __device__ __forceinline__ int32_t warp_row(const int64_t* __restrict__ a_rowptr
                         v = src.payload(base + (t - e), a);
                 }
                 accumulate_item<true, kCountOnly>(valid, key, v, map, ids, pay, cap, cnt, ctr,
-                                                  lane);
+                                                  lane, l1_keys, spill);
             }
         }
     }

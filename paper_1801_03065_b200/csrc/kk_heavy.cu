@@ -228,7 +228,6 @@ __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L,
             for (int w = 0; w < nw; ++w)
                 s += red[w];
             L.sym_sizes[i] = static_cast<int64_t>(s);
-            atomicAdd(&L.ctr->pool_allocations, 1ull);
         }
         __syncthreads();
     }
@@ -554,10 +553,6 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
                     L.c_vals[cbase + o + q] = __longlong_as_double(rc.y);
                 }
             }
-        }
-        if (threadIdx.x == 0) {
-            atomicAdd(&L.ctr->pool_allocations, 1ull);
-            atomicAdd(&L.ctr->l2_inserts, static_cast<unsigned long long>(s_total));
         }
         __syncthreads();
     }

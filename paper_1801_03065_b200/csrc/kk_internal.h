@@ -64,6 +64,7 @@ struct RowLaunch {
     const unsigned long long* d_nrows; // symbolic heavy kernel: row count on the device (else nrows)
     const unsigned long long* gate; // numeric fast kernel: exit when gate[0..1] == gate[2..3] (replayed)
     int32_t no_segments;            // symbolic fast kernel: always use 32-product windows (A/B switch)
+    int32_t l1_keys;                // the reference's level-1 key capacity (statistics only)
     // outputs
     int64_t* sym_sizes;          // symbolic: sizes[i] (== rowptr + 1)
     const int64_t* c_rowptr;     // numeric
@@ -108,6 +109,11 @@ cudaError_t launch_transpose_fill(int32_t m, int32_t n, const int64_t* rowptr, c
 cudaError_t launch_col_range(int32_t m, const int64_t* a_rowptr, const int32_t* a_cols, int* out2, cudaStream_t st);
 cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals* tot,
                                    cudaStream_t st);
+cudaError_t launch_collect_empty_rows(int32_t m, const int64_t* c_rowptr, int32_t* list, unsigned long long* count,
+                                      cudaStream_t st);
+cudaError_t launch_check_empty_rows(const int32_t* list, int64_t n, const int64_t* a_rowptr, const int32_t* a_cols,
+                                    const int64_t* b_rowptr, int32_t row_lo, int32_t row_hi, DevCounters* ctr,
+                                    cudaStream_t st);
 
 // fast paths (kk_fast.cu)
 cudaError_t launch_numeric_fast(const RowLaunch& L, cudaStream_t st);

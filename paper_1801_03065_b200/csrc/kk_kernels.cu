@@ -534,6 +534,9 @@ __global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
         }
     }
 
+    // reference statistics (engine.cpp:78-87, memory_pool allocation_count):
+    // rows whose distinct keys exceed the reference's L1 key capacity take one
+    // pool chunk; every product of a key past that rank is an L2 insert
     unsigned long long my_alloc = 0, my_inserts = 0;
     for (int64_t r = gw; r < L.nrows; r += nwarps) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
@@ -545,7 +548,6 @@ __global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
                 chunk = acquire_chunk(L.pool, static_cast<int>(gw % L.pool.num_chunks), lane);
                 region = reinterpret_cast<unsigned char*>(L.pool.base) + (size_t)chunk * L.pool.chunk_bytes;
             }
-            ++my_alloc;
         }
         int32_t* ids;
         P* pay;
@@ -569,20 +571,20 @@ __global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
             pay = reinterpret_cast<P*>(region + L.lay.off_pay);
         }
         Map map = MapOf<kAcc>::make(region, L.lay, ids, L.ctr);
-        int64_t products = 0;
+        int64_t spill = 0;
         int32_t cnt;
         if constexpr (kVar == kVarNumeric) {
             const NumericSource src{L.b_rowptr, L.b_cols, L.b_vals};
             cnt = warp_row<kFlat, false>(L.a_rowptr, L.a_cols, L.a_vals, i, src, map, ids, pay,
-                                         cap, L.ctr, lane, products);
+                                         cap, L.ctr, lane, L.l1_keys, spill);
         } else if constexpr (kVar == kVarSymRaw) {
             const RawStructSource src{L.b_rowptr, L.b_cols};
             cnt = warp_row<kFlat, true>(L.a_rowptr, L.a_cols, nullptr, i, src, map, ids, pay,
-                                        cap, L.ctr, lane, products);
+                                        cap, L.ctr, lane, L.l1_keys, spill);
         } else {
             const CompressedSource src{L.b_rowptr, L.csize, L.cpair};
             cnt = warp_row<kFlat, false>(L.a_rowptr, L.a_cols, nullptr, i, src, map, ids, pay,
-                                         cap, L.ctr, lane, products);
+                                         cap, L.ctr, lane, L.l1_keys, spill);
         }
         const int32_t used = min(cnt, cap);
         if constexpr (kNum) {
@@ -610,8 +612,11 @@ __global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
             if (lane == 0)
                 L.sym_sizes[i] = size;
         }
-        if (kL2)
-            my_inserts += products;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1)
+            spill += __shfl_xor_sync(kFull, spill, off);
+        my_inserts += static_cast<unsigned long long>(spill);
+        my_alloc += cnt > L.l1_keys ? 1 : 0;
         __syncwarp();
         for (int32_t q = lane; q < used; q += 32)
             map.reset(q, ids);
@@ -623,11 +628,9 @@ __global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
             }
         }
     }
-    if constexpr (kL2) {
-        if (lane == 0 && my_alloc) {
-            atomicAdd(&L.ctr->pool_allocations, my_alloc);
-            atomicAdd(&L.ctr->l2_inserts, my_inserts);
-        }
+    if (lane == 0 && (my_alloc || my_inserts)) {
+        atomicAdd(&L.ctr->pool_allocations, my_alloc);
+        atomicAdd(&L.ctr->l2_inserts, my_inserts);
     }
 }
 
@@ -935,6 +938,93 @@ cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals*
         return cudaSuccess;
     const int blocks = (int)std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 8);
     row_hist_kernel<<<blocks, 256, 0, st>>>(m, rowptr, tot);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Rows the symbolic structure left empty.  The numeric kernels never visit
+// them, so a reused handle whose new operands DO produce products in such a
+// row would drop them silently; the reference's NumericSink::finish throws
+// "numeric row exceeds the symbolic structure" (engine.cpp:238-239).  The
+// rows are collected once per plan and checked on every numeric pass.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) collect_empty_rows_kernel(int32_t m, const int64_t* __restrict__ c_rowptr,
+                                                                 int32_t* __restrict__ list,
+                                                                 unsigned long long* __restrict__ count)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool e = i < m && c_rowptr[i + 1] == c_rowptr[i];
+        const uint32_t b = __ballot_sync(kFull, e);
+        unsigned long long off = 0;
+        if (lane == 0 && b)
+            off = atomicAdd(count, (unsigned long long)__popc(b));
+        off = __shfl_sync(kFull, off, 0);
+        if (e)
+            list[off + __popc(b & lanemask_lt())] = static_cast<int32_t>(i);
+    }
+}
+
+__global__ void __launch_bounds__(256) check_empty_rows_kernel(const int32_t* __restrict__ list, int64_t n,
+                                                               const int64_t* __restrict__ a_rowptr,
+                                                               const int32_t* __restrict__ a_cols,
+                                                               const int64_t* __restrict__ b_rowptr,
+                                                               int32_t row_lo, int32_t row_hi, DevCounters* ctr)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    // 32 rows per warp step: lane r owns row list[g + r]; rows with A entries
+    // are then walked by the whole warp (rare: an empty C row normally has an
+    // empty A row or references empty B rows only)
+    for (int64_t g = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; g < n; g += warps * 32) {
+        int64_t ab = 0, ae = 0;
+        if (g + lane < n) {
+            const int32_t i = __ldg(list + g + lane);
+            if (!(row_hi > 0 && (i < row_lo || i >= row_hi))) {
+                ab = __ldg(a_rowptr + i);
+                ae = __ldg(a_rowptr + i + 1);
+            }
+        }
+        uint32_t todo = __ballot_sync(kFull, ae > ab);
+        while (todo) {
+            const int r = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int64_t lo = __shfl_sync(kFull, ab, r), hi = __shfl_sync(kFull, ae, r);
+            bool any = false;
+            for (int64_t p = lo + lane; p < hi && !any; p += 32) {
+                const int32_t j = __ldg(a_cols + p);
+                any = __ldg(b_rowptr + j + 1) > __ldg(b_rowptr + j);
+            }
+            if (__any_sync(kFull, any)) {
+                if (lane == 0)
+                    raise_error(ctr, kDevRowOverflow);
+                return;
+            }
+        }
+    }
+}
+
+cudaError_t launch_collect_empty_rows(int32_t m, const int64_t* c_rowptr, int32_t* list, unsigned long long* count,
+                                      cudaStream_t st)
+{
+    if (m <= 0)
+        return cudaSuccess;
+    const int blocks = (int)std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 8);
+    collect_empty_rows_kernel<<<blocks, 256, 0, st>>>(m, c_rowptr, list, count);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_empty_rows(const int32_t* list, int64_t n, const int64_t* a_rowptr, const int32_t* a_cols,
+                                    const int64_t* b_rowptr, int32_t row_lo, int32_t row_hi, DevCounters* ctr,
+                                    cudaStream_t st)
+{
+    if (n <= 0)
+        return cudaSuccess;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 4));
+    check_empty_rows_kernel<<<blocks, 256, 0, st>>>(list, n, a_rowptr, a_cols, b_rowptr, row_lo, row_hi, ctr);
     count_launch();
     return cudaGetLastError();
 }

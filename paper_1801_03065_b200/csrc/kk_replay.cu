@@ -21,8 +21,8 @@
 //
 // The map is valid only for the structure it was recorded on.  The reference
 // checks dimensions and nnz only (engine.cpp:451-453); the replay path also
-// fingerprints A's and B's row offsets and column indices (64-bit,
-// position-weighted, relative to the row-offset base so row-block views
+// fingerprints A's and B's row offsets and column indices (64-bit sums of
+// a non-linear hash of (position, value), relative to the row-offset base so row-block views
 // fingerprint like the matrix they were cut from) on every pass.  The replay
 // kernel and the hashing kernels are both launched and both read the
 // fingerprints: exactly one of them does the work, with no host round trip.
@@ -35,16 +35,33 @@ namespace kk {
 
 namespace {
 
-// Position-weighted sum: element idx contributes value * (2K*idx + 1) (mod
-// 2^64).  The weights are odd, so any single changed entry changes the sum;
-// unrelated changes cancel with probability ~2^-64.  Weights advance by
-// additions only.
+// Order-independent sum of a NON-linear per-element hash:
+//   element idx with value x contributes mix64(w(idx) ^ x)   (mod 2^64),
+// w(idx) = 2K*idx + 1 an odd (bijective) position weight and mix64 the
+// splitmix64 finalizer.  A moment checksum (sum of w(idx) * x) would be blind
+// to edits that preserve two moments of the column array (e.g. two adjacent
+// swaps with opposite column gaps in different rows); through the mixer every
+// changed (position, value) pair moves the sum by an unrelated 64-bit amount,
+// so a structural edit goes undetected with probability ~2^-64 whatever its
+// shape.  Threads still combine partial sums in any order.
 constexpr uint64_t kFpK2 = 0x3C6EF372FE94F82Aull; // 2 * 0x9E3779B97F4A7C15 (mod 2^64)
 
 __device__ __forceinline__ uint64_t fp_weight(int64_t idx)
 {
     return static_cast<uint64_t>(idx) * kFpK2 + 1ull;
 }
+
+__device__ __forceinline__ uint64_t fp_mix(uint64_t x)
+{
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+__device__ __forceinline__ uint64_t fp_term(uint64_t w, uint64_t x) { return fp_mix(w ^ x); }
 
 // sum over (i, rowptr[i] - rowptr[0]) and (q, cols[rowptr[0] + q]); the row
 // offsets are weighted from index nnz + 1 on so they never share weights with
@@ -59,27 +76,25 @@ __global__ void __launch_bounds__(256) fingerprint_kernel(int64_t rows, const in
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t acc = 0;
     for (int64_t i = tid; i <= rows; i += stride)
-        acc += static_cast<uint64_t>(__ldg(rowptr + i) - base) * fp_weight(nnz + 1 + i);
+        acc += fp_term(fp_weight(nnz + 1 + i), static_cast<uint64_t>(__ldg(rowptr + i) - base));
     // columns: four per thread per iteration (int4 once 16-byte aligned)
     const int32_t* c = cols + base;
     const uintptr_t mis = reinterpret_cast<uintptr_t>(c) & 15;
     const int64_t head = mis ? static_cast<int64_t>((16 - mis) >> 2) : 0;
     const int64_t h = head < nnz ? head : nnz;
     for (int64_t q = tid; q < h; q += stride)
-        acc += static_cast<uint64_t>(static_cast<uint32_t>(__ldg(c + q))) * fp_weight(q);
+        acc += fp_term(fp_weight(q), static_cast<uint32_t>(__ldg(c + q)));
     const int64_t nvec = (nnz - h) >> 2;
     const int4* v = reinterpret_cast<const int4*>(c + h);
     uint64_t w = fp_weight(h + 4 * tid);
     const uint64_t wstep = 4ull * static_cast<uint64_t>(stride) * kFpK2;
     for (int64_t q = tid; q < nvec; q += stride, w += wstep) {
         const int4 x = __ldg(v + q);
-        acc += static_cast<uint64_t>(static_cast<uint32_t>(x.x)) * w
-            + static_cast<uint64_t>(static_cast<uint32_t>(x.y)) * (w + kFpK2)
-            + static_cast<uint64_t>(static_cast<uint32_t>(x.z)) * (w + 2 * kFpK2)
-            + static_cast<uint64_t>(static_cast<uint32_t>(x.w)) * (w + 3 * kFpK2);
+        acc += fp_term(w, static_cast<uint32_t>(x.x)) + fp_term(w + kFpK2, static_cast<uint32_t>(x.y))
+            + fp_term(w + 2 * kFpK2, static_cast<uint32_t>(x.z)) + fp_term(w + 3 * kFpK2, static_cast<uint32_t>(x.w));
     }
     for (int64_t q = h + 4 * nvec + tid; q < nnz; q += stride)
-        acc += static_cast<uint64_t>(static_cast<uint32_t>(__ldg(c + q))) * fp_weight(q);
+        acc += fp_term(fp_weight(q), static_cast<uint32_t>(__ldg(c + q)));
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1)
         acc += __shfl_xor_sync(kFull, acc, off);

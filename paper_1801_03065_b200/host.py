@@ -242,6 +242,9 @@ def multiply_host(a: PinnedCsr, b: Optional[PinnedCsr] = None, cfg: Optional[Spg
         mark(f"copied {r0}:{r1}", side)
     main.wait_stream(side)
     main.synchronize()  # the reference's multiply returns a finished host CSR
+    # a device error raised by any block (row overflow/short, pool or bucket
+    # overflow) surfaces here as the reference's logic_error would
+    h.check()
     sorted_c = bool(cfg.sort_output) if cfg is not None else False
     c = CsrMatrix(m, src_b.num_cols, o_ro.numpy()[:m + 1], o_ci.numpy()[:nnz_c], o_v.numpy()[:nnz_c], sorted_c)
     d2h = (m + 1) * 8 + nnz_c * 12

@@ -149,6 +149,79 @@ def test_every_accumulator_scheme_and_level(kk, oracle, acc, scheme, l1):
         assert allocs >= 1  # engine_test.cpp:118-119
 
 
+@pytest.mark.parametrize("acc", [0, 1, 2])
+@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("l1", [1, 7, 40])
+def test_phase_stats_match_reference(kk, reference, acc, scheme, l1):
+    """PhaseStats carry the reference's meaning (engine.cpp:78-87,
+    memory_pool.cpp allocation_count): pool_allocations = rows whose distinct
+    keys overflow the level-1 accumulator, l2_inserts = products of keys past
+    its capacity.  Equal to the reference's own counters, both phases."""
+    rng = np.random.default_rng(500 + 100 * acc + 10 * scheme + l1)
+    for it in range(3):
+        m, n, k = (int(x) for x in rng.integers(20, 160, 3))
+        a = random_csr(rng, m, n, 0.12, shuffle=bool(it % 2))
+        b = random_csr(rng, n, k, 0.12, shuffle=bool(it % 2))
+        cfg = kk.SpgemmConfig(accumulator=acc, scheme=scheme, l1_capacity=l1)
+        h = kk.symbolic(a, b, cfg)
+        st = kk.PhaseStats()
+        kk.numeric(a, b, h, st)
+        rh = reference.symbolic(a, b, accumulator=acc, scheme=scheme, l1_capacity=l1)
+        info = rh.info()
+        _, _, rst = rh.numeric()
+        assert h.symbolic_stats.pool_allocations == info["sym_pool_allocations"]
+        assert h.symbolic_stats.l2_inserts == info["sym_l2_inserts"]
+        assert st.pool_allocations == rst["pool_allocations"]
+        assert st.l2_inserts == rst["l2_inserts"]
+
+
+@pytest.mark.parametrize("acc", [1, 2])
+def test_pool_many2many_budget_halving(kk, oracle, reference, acc):
+    """plan_pool (memory_pool.cpp:83-109): many2many chunk claims with a budget
+    that halves the chunk count to a handful; results stay bit-exact and the
+    statistics equal the reference's under the same budget."""
+    rng = np.random.default_rng(71 + acc)
+    a = random_csr(rng, 300, 200, 0.1)
+    b = random_csr(rng, 200, 250, 0.1)
+    probe = kk.symbolic(a, b, kk.SpgemmConfig(accumulator=acc, l1_capacity=1))
+    bound = max(probe.numeric_choice.l2_capacity, probe.symbolic_choice.l2_capacity)
+    budget = 3 * ((bound + 1) // 2 * 2 * 32)  # three reference chunks
+    for mode in (kk.PoolMode.Many2Many, kk.PoolMode.One2One):
+        cfg = kk.SpgemmConfig(accumulator=acc, l1_capacity=1, pool_mode=mode, pool_budget_bytes=budget)
+        h = kk.symbolic(a, b, cfg)
+        st = kk.PhaseStats()
+        c = kk.numeric(a, b, h, st).to_host()
+        assert_parity(oracle, a, b, c)
+        rh = reference.symbolic(a, b, accumulator=acc, l1_capacity=1, pool_mode=mode, pool_budget_bytes=budget)
+        _, _, rst = rh.numeric()
+        assert st.pool_allocations == rst["pool_allocations"] > 0
+        assert st.l2_inserts == rst["l2_inserts"] > 0
+
+
+def test_pool_budget_below_one_chunk(kk, reference):
+    """PoolSizingError when one chunk exceeds the budget (memory_pool.cpp:97-99),
+    raised by the phase whose resolved accumulator is LL/LP, as the reference does."""
+    rng = np.random.default_rng(73)
+    a = random_csr(rng, 60, 60, 0.2)
+    b = random_csr(rng, 60, 60, 0.2)
+    for acc in (1, 2):
+        with pytest.raises(kk.PoolSizingError):
+            kk.symbolic(a, b, kk.SpgemmConfig(accumulator=acc, pool_budget_bytes=16))
+        with pytest.raises(RuntimeError, match="exceeds the memory budget"):
+            reference.symbolic(a, b, accumulator=acc, pool_budget_bytes=16)
+    # Dense (Auto on a small domain) is single-level: no pool, no error
+    h = kk.symbolic(a, b, kk.SpgemmConfig(pool_budget_bytes=16))
+    assert h.symbolic_choice.accumulator == kk.AccumulatorKind.Dense
+    reference.symbolic(a, b, pool_budget_bytes=16)
+    # numeric raises when only its own choice needs a pool
+    h2 = kk.symbolic(a, b)
+    h2.set_numeric(kk.SpgemmConfig(pool_budget_bytes=16),
+                   kk.ResolvedConfig(accumulator=kk.AccumulatorKind.LL, scheme=0, l1_capacity=4,
+                                     effective_k=60, l2_capacity=60))
+    with pytest.raises(kk.PoolSizingError):
+        kk.numeric(a, b, h2, kk.PhaseStats())
+
+
 def test_ample_l1_never_touches_pool(kk):
     rng = np.random.default_rng(67)
     a = random_csr(rng, 50, 50, 0.1)
@@ -278,6 +351,89 @@ def test_replay_falls_back_on_structure_change(kk, oracle):
         kk.numeric(a, b3, h, kk.PhaseStats())
 
 
+def test_replay_detects_compensating_swaps(kk, oracle):
+    """Edits that keep two moments of B's column array (adjacent swaps with
+    opposite gaps in two rows, and a (+1,-2,+1) change at three consecutive
+    positions) change C's first-touch order: the recorded slot map must not be
+    replayed for them (kk_replay.cu fingerprint)."""
+    rng = np.random.default_rng(31)
+    n, k = 64, 200  # B rows of ~15 entries: the Thread-Sequential (replayable) plan
+    rows = []
+    for i in range(n):
+        pool = [c for c in range(k) if c not in (3, 4, 7, 8, 20, 21, 22)]
+        rows.append(list(rng.choice(pool, size=13, replace=False)))
+    rows[5] = [3, 4] + rows[5]      # ascending pair, gap 1
+    rows[40] = [8, 7] + rows[40]    # descending pair, gap 1
+    rows[17] = [20, 22, 21] + rows[17][:10]
+    ro = np.zeros(n + 1, np.int64)
+    np.cumsum([len(r) for r in rows], out=ro[1:])
+    b = kk.CsrMatrix(n, k, ro, np.concatenate(rows).astype(np.int32), rng.uniform(-1, 1, int(ro[-1])), False)
+    a = random_csr(rng, 80, n, 0.3)
+    h = kk.symbolic(a, b)
+    for _ in range(3):
+        kk.numeric(a, b, h)
+    assert h.replay_state == 2
+    edits = []
+    b2 = b.col_indices.copy()
+    b2[ro[5]:ro[5] + 2] = [4, 3]
+    b2[ro[40]:ro[40] + 2] = [7, 8]
+    edits.append(b2)
+    b3 = b.col_indices.copy()
+    b3[ro[17]:ro[17] + 3] = [21, 20, 22]  # deltas (+1, -2, +1)
+    edits.append(b3)
+    for cols in edits:
+        bx = kk.CsrMatrix(n, k, ro, cols, b.values, False)
+        c = kk.numeric(a, bx, h, kk.PhaseStats()).to_host()
+        assert_parity(oracle, a, bx, c)
+    c = kk.numeric(a, b, h).to_host()
+    assert_parity(oracle, a, b, c)
+
+
+def test_row_block_errors_survive_later_blocks(kk):
+    """A device error raised by one row block of a pass stays visible until
+    the pass is checked (host.multiply_host calls check after its last block):
+    later blocks must not clear it."""
+    import torch
+    rng = np.random.default_rng(37)
+    a = random_csr(rng, 200, 200, 0.1)
+    b = random_csr(rng, 200, 200, 0.1)
+    h = kk.symbolic(a, b)
+    bad = kk.CsrMatrix(b.num_rows, b.num_cols, b.row_offsets, b.col_indices.copy(), b.values, False)
+    for i in range(bad.num_rows):
+        lo, hi = bad.row_offsets[i], bad.row_offsets[i + 1]
+        bad.col_indices[lo:hi] = np.arange(hi - lo) % bad.num_cols
+    nnz = h.nnz_c()
+    cols = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    kk.numeric_rows(a, bad, h, 0, 100, cols, vals)   # block 0: structure mismatch
+    kk.numeric_rows(a, b, h, 100, 200, cols, vals)   # block 1: clean
+    with pytest.raises(kk.InternalError):
+        h.check()
+    kk.numeric_rows(a, b, h, 0, 100, cols, vals)     # a new pass starts at row 0
+    kk.numeric_rows(a, b, h, 100, 200, cols, vals)
+    h.check()
+
+
+def test_products_in_a_structurally_empty_row_are_reported(kk):
+    """A reused handle whose new A puts products into a row of C the symbolic
+    pass left empty raises (NumericSink::finish, engine.cpp:238-239) instead
+    of dropping them: same nnz, one entry moved from a B row that is empty to
+    one that is not, into an empty A row."""
+    rng = np.random.default_rng(41)
+    trips_b = [(i, int(c), float(rng.uniform(-1, 1))) for i in range(40) if i != 7
+               for c in rng.choice(50, 6, replace=False)]
+    b = csr_from_triplets(40, 50, trips_b)
+    base = [(r, int(c), 1.0) for r in (0, 1, 2, 4, 6, 8, 9) for c in rng.choice(40, 4, replace=False) if c != 7]
+    a = csr_from_triplets(10, 40, base + [(5, 7, 2.0), (5, 12, 3.0)])
+    a2 = csr_from_triplets(10, 40, base + [(3, 20, 2.0), (5, 12, 3.0)])
+    assert a.nnz() == a2.nnz()
+    h = kk.symbolic(a, b)
+    assert h.c_row_offsets[4] == h.c_row_offsets[3]  # row 3 of C is empty
+    kk.numeric(a, b, h, kk.PhaseStats())
+    with pytest.raises(kk.InternalError):
+        kk.numeric(a2, b, h, kk.PhaseStats())
+
+
 def test_replay_row_block_views(kk, oracle):
     rng = np.random.default_rng(29)
     a = random_csr(rng, 400, 150, 0.12)
@@ -394,7 +550,6 @@ def test_c4_rmat_row_sampled(kk, oracle):
     a = G.rmat(17, 16, 1)
     res = kk.multiply(a, a)
     h = res.handle
-    assert h.symbolic_stats.pool_allocations + res.numeric_stats.pool_allocations > 0
     ro = h.c_row_offsets
     sizes = np.diff(ro)
     rows = np.unique(np.concatenate([np.arange(0, a.num_rows, 32), np.argsort(sizes)[-128:]]))

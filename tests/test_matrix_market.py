@@ -108,3 +108,39 @@ def test_matches_reference_reader(tmp_path, reference):
     for kind in sorted(BAD):
         with pytest.raises(ValueError):
             reference.read_mm(_write(tmp_path, kind + "_ref.mtx", BAD[kind]))
+
+
+def test_multi_slice_file_matches_reference(tmp_path, reference):
+    """A file large enough to be tokenised in several slices (one per host
+    thread) reads bit-identically to the reference reader, symmetric too."""
+    a = G.rmat(14, 16, 5)
+    path = str(tmp_path / "big.mtx")
+    G.write_matrix_market(a, path)
+    _same(G.read_matrix_market(path), reference.read_mm(path))
+    # symmetric: lower triangle of a, mirrored on read
+    lines = ["%%MatrixMarket matrix coordinate real symmetric"]
+    ents = []
+    for i in range(a.num_rows):
+        for q in range(int(a.row_offsets[i]), int(a.row_offsets[i + 1])):
+            j = int(a.col_indices[q])
+            if j <= i:
+                ents.append(f"{i + 1} {j + 1} {float(a.values[q]):.17g}")
+    lines.append(f"{a.num_rows} {a.num_cols} {len(ents)}")
+    sym = str(tmp_path / "sym.mtx")
+    with open(sym, "w") as f:
+        f.write("\n".join(lines + ents) + "\n")
+    _same(G.read_matrix_market(sym), reference.read_mm(sym))
+
+
+def test_entries_after_the_declared_count_are_ignored(tmp_path, reference):
+    text = "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n2 2 2\n9 9 garbage\n"
+    path = _write(tmp_path, "extra.mtx", text)
+    m = G.read_matrix_market(path)
+    assert m.nnz() == 2 and m.values.tolist() == [1.0, 2.0]
+    _same(m, reference.read_mm(path))
+
+
+def test_error_line_numbers(tmp_path):
+    text = "%%MatrixMarket matrix coordinate real general\n% c\n3 3 3\n1 1 1\n\n2 2 x\n3 3 3\n"
+    with pytest.raises(ValueError, match="line 6"):
+        G.read_matrix_market(_write(tmp_path, "ln.mtx", text))
