@@ -136,6 +136,9 @@ typedef struct spg_handle_info {
     const int64_t* d_per_row_flops; /* [m], device, owned by the handle   */
     int64_t compressed_nnz_b;       /* (word index, bits) pairs of the compressed B
                                        rows A references (compress_rows output size) */
+    int32_t heavy_path;             /* rows beyond the warp tables: 0 none, 1 hashed
+                                       buckets, 2 column slabs (diagnostic) */
+    int32_t b_sorted;               /* symbolic saw every referenced B row sorted */
 } spg_handle_info;
 
 typedef struct spg_handle* spg_handle_t;

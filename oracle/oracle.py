@@ -386,3 +386,28 @@ class RefHandle:
             raise RuntimeError(f"ref numeric failed ({rc}): {self.ref.L.ref_last_error().decode()}")
         return cols[:nnz], vals[:nnz], {"ms": st.ms, "pool_allocations": st.pool_allocations,
                                         "l2_inserts": st.l2_inserts}
+
+
+GEN_SO = os.path.join(HERE, "libgen.so")
+
+
+def generators():
+    """The BASELINE input generators built by the oracle Makefile from the same
+    source as the product's (csrc/generators.cpp): bench.py's reference arm
+    creates its inputs with these, so its process loads no product library."""
+    if not os.path.exists(GEN_SO):
+        subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
+    from paper_1801_03065_b200.generators import Generators
+    return Generators(GEN_SO)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"

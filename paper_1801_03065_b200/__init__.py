@@ -141,7 +141,7 @@ class _Info(C.Structure):
                 ("symbolic_choice", _Resolved), ("numeric_choice", _Resolved),
                 ("config", _Config), ("symbolic_stats", _PhaseStats), ("compress_ms", C.c_double),
                 ("d_c_row_offsets", C.c_void_p), ("d_per_row_flops", C.c_void_p),
-                ("compressed_nnz_b", C.c_int64)]
+                ("compressed_nnz_b", C.c_int64), ("heavy_path", C.c_int32), ("b_sorted", C.c_int32)]
 
 
 class _Desc(C.Structure):
@@ -408,6 +408,11 @@ class SpgemmHandle:
     def replay_state(self) -> int:
         """0 hashing only, 1 replay eligible, 2 slot map recorded (kk_replay.cu)."""
         return int(lib().spg_handle_replay_state(self._ptr))
+    @property
+    def heavy_path(self) -> int:
+        """Rows beyond the warp tables: 0 none, 1 hashed buckets, 2 column slabs."""
+        return int(self._info().heavy_path)
+
     @property
     def avg_row_size(self): return float(self._info().avg_row_size)
     @property

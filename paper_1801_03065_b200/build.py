@@ -45,11 +45,12 @@ def _stale(target: str, sources: list[str]) -> bool:
 
 
 def build_kkspgemm(force: bool = False, verbose: bool = False) -> str:
-    srcs = [os.path.join(CSRC, f) for f in ("kk_api.cu", "kk_kernels.cu", "kk_fast.cu", "kk_heavy.cu", "kk_replay.cu")]
+    srcs = [os.path.join(CSRC, f) for f in ("kk_api.cu", "kk_kernels.cu", "kk_fast.cu", "kk_heavy.cu", "kk_slab.cu", "kk_replay.cu")]
     deps = srcs + [os.path.join(CSRC, f) for f in ("kk_device.cuh", "kk_internal.h")] + [
         os.path.join(ROOT, "include", "kkspgemm.h")]
     if force or _stale(LIB, deps):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *srcs, "-o", LIB]
+        extra = os.environ.get("KK_NVCC_DEFS", "").split()  # e.g. -DKK_SLAB_PROF (profiling builds)
+        cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *srcs, "-o", LIB]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)

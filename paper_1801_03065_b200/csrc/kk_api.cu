@@ -542,6 +542,8 @@ const char* dev_error_text(int code)
     case kDevKeyRange: return "DenseAccumulator: key outside the column domain";
     case kDevL2Overflow: return "level-2 accumulator overflow: chunk bound violated";
     case kDevReplay: return "slot replay does not match the structure";
+    case kDevUnsorted:
+        return "B row not column-sorted: the column-slab plan of this handle needs sorted B rows (run symbolic on this B)";
     default: return "device error";
     }
 }
@@ -566,6 +568,11 @@ struct spg_handle {
     cudaStream_t stream = nullptr;
     // heavy numeric rows (kk_heavy.cu): per-CTA staging for the bucket scatter
     bool num_heavy = false;
+    bool num_slab = false;      // heavy rows by column slabs (kk_slab.cu) instead of buckets
+    bool b_sorted = false;      // symbolic saw every referenced B row column-sorted
+    int64_t max_a_row = 0;      // longest A row (slab cursors)
+    int32_t* slab_scratch = nullptr;
+    int slab_grid = 0;
     int heavy_nb = 0;
     int64_t heavy_stage = 0; // staging products
     int64_t heavy_cap = 0;
@@ -605,6 +612,8 @@ struct spg_handle {
         free_replay();
         if (heavy_stage_buf)
             cudaFree(heavy_stage_buf);
+        if (slab_scratch)
+            cudaFree(slab_scratch);
         if (d_rowptr)
             cudaFree(d_rowptr);
         if (d_prf)
@@ -648,7 +657,16 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
     // when a row's distinct columns fit the hashed buckets and its products
     // fit 32-bit staging offsets
     h->num_heavy = false;
-    if (fast && !forced && h->num.l2_class >= 0) {
+    h->num_slab = false;
+    if (fast && !forced && h->num.l2_class >= 0 && h->b_sorted && h->max_a_row > 0) {
+        // column slabs: no row-size limit, products read once
+        h->num_heavy = true;
+        h->num_slab = true;
+        h->slab_grid = numeric_slab_blocks_per_sm() * sm_count();
+        if (h->slab_scratch)
+            cudaFreeAsync(h->slab_scratch, st);
+        h->slab_scratch = dalloc<int32_t>(static_cast<size_t>(h->slab_grid) * 2 * h->max_a_row, st, "slab cursors");
+    } else if (fast && !forced && h->num.l2_class >= 0) {
         const int64_t cap = std::max<int64_t>(h->info.flops.max_row_flops, 1);
         if (h->info.max_row_size <= kHeavyMaxRow && cap < (int64_t{1} << 31)) {
             h->num_heavy = true;
@@ -961,15 +979,22 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         // ---- K3 + K1/K4 ----
         const int32_t j0 = std::clamp(hcrange[0], 0, n), j1 = std::clamp(hcrange[1] + 1, j0, n);
         cudaFreeAsync(d_crange, st);
-        cuda_check(launch_compress(j1 - j0, b->row_offsets + j0, b->col_indices, d_csize + j0, d_cp, &d_tot->nnz_bc, st),
+        cuda_check(launch_compress(j1 - j0, b->row_offsets + j0, b->col_indices, d_csize + j0, d_cp, &d_tot->nnz_bc,
+                                   &d_tot->unsorted, st),
                    "compress");
         const double avg_len = m > 0 ? static_cast<double>(a->nnz) / m : 0.0;
         cuda_check(launch_flops(m, avg_len, a->row_offsets, a->col_indices, b->row_offsets, d_csize,
                                 h->d_prf, d_prcf, d_tot, st),
                    "flops");
+        // longest A row (cursor arrays of the column-slab kernel)
+        cuda_check(launch_row_bucket_hist(m, a->row_offsets, d_stot, st), "A row lengths");
         cuda_check(cudaMemcpyAsync(htot, d_tot, sizeof(Totals), cudaMemcpyDeviceToHost, st), "totals");
+        cuda_check(cudaMemcpyAsync(hstot, d_stot, sizeof(ScanTotals), cudaMemcpyDeviceToHost, st), "A totals");
+        cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");
         cuda_check(cudaEventRecord(ev[1], st), "event");
         cuda_check(cudaStreamSynchronize(st), "flops sync");
+        h->max_a_row = static_cast<int64_t>(hstot->max_size);
+        h->b_sorted = htot->unsorted == 0;
 
         // ---- host decisions (engine.cpp:409-423, compression.cpp:118-147) ----
         I.flops.total_flops = static_cast<int64_t>(htot->total_f);
@@ -1250,7 +1275,11 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
             L.wpb = pc.wpb;
             L.grid = pc.grid;
             L.l2 = pc.l2;
-            if (pc.l2 && h->num_heavy) {
+            if (pc.l2 && h->num_slab) {
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(h->slab_grid, pc.count)));
+                cuda_check(launch_numeric_slab(L, h->slab_scratch, h->max_a_row, I.k, h->d_prf, grid, st),
+                           "numeric slab kernel");
+            } else if (pc.l2 && h->num_heavy) {
                 const int64_t resident = int64_t{numeric_heavy_blocks_per_sm(h->heavy_nb)} * sm_count();
                 const int64_t want = std::max<int64_t>(1, std::min<int64_t>(resident, pc.count));
                 if (!h->heavy_stage_buf) {
@@ -1332,6 +1361,8 @@ int spg_handle_info_get(spg_handle_t h, spg_handle_info* out)
     if (!h || !out)
         return SPG_ERR_CONTRACT;
     *out = h->info;
+    out->heavy_path = h->num_slab ? 2 : h->num_heavy ? 1 : 0;
+    out->b_sorted = h->b_sorted ? 1 : 0;
     return SPG_OK;
 }
 

@@ -33,6 +33,7 @@ enum DevError : int {
     kDevKeyRange = 3,     // key outside the dense domain (accumulators.hpp:308-309)
     kDevL2Overflow = 4,   // level-2 bound violated (engine.cpp:83-84)
     kDevReplay = 5,       // slot-replay map does not match the structure (kk_replay.cu)
+    kDevUnsorted = 6,     // column-slab path met a B row that is not column-sorted (kk_slab.cu)
 };
 
 struct DevCounters {

@@ -30,6 +30,7 @@ TabLayout make_layout(int acc, int variant, int32_t S, int32_t domain, double oc
 struct Totals {
     unsigned long long total_f, max_f, total_cf, max_cf;
     unsigned long long nnz_bc; // compressed pairs written (the compress pass)
+    unsigned long long unsorted; // > 0: some compressed B row is not strictly column-sorted
     unsigned long long hist_f[64];
     unsigned long long hist_cf[64];
 };
@@ -81,7 +82,8 @@ struct RowLaunch {
 
 // kernel launchers (kk_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
-                            int32_t* csize, int2* cp, unsigned long long* nnz_bc, cudaStream_t st);
+                            int32_t* csize, int2* cp, unsigned long long* nnz_bc, unsigned long long* unsorted,
+                            cudaStream_t st);
 cudaError_t launch_flops(int32_t m, double avg_len, const int64_t* a_rowptr,
                          const int32_t* a_cols, const int64_t* b_rowptr, const int32_t* csize,
                          int64_t* out_f, int64_t* out_cf, Totals* tot, cudaStream_t st);
@@ -131,6 +133,11 @@ cudaError_t launch_numeric_heavy(const RowLaunch& L, void* stage, int64_t stage_
                                  int queue, int grid, cudaStream_t st);
 cudaError_t sort_rows_by_flops_desc(int32_t* list, int64_t n, const int64_t* prf, cudaStream_t st);
 int numeric_heavy_blocks_per_sm(int32_t nb);
+
+// heavy rows by column slabs (kk_slab.cu); needs column-sorted B rows
+cudaError_t launch_numeric_slab(const RowLaunch& L, int32_t* scratch, int64_t max_a_row, int64_t k,
+                                const int64_t* prf, int grid, cudaStream_t st);
+int numeric_slab_blocks_per_sm();
 
 // structure-reuse replay (kk_replay.cu)
 struct ReplayLaunch {

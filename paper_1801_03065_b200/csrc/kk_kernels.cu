@@ -92,10 +92,12 @@ constexpr int32_t kShortRow = 8;
 __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                              const int32_t* __restrict__ cols,
                                                              int32_t* __restrict__ csize,
-                                                             int2* __restrict__ cp, unsigned long long* nnz_bc)
+                                                             int2* __restrict__ cp, unsigned long long* nnz_bc,
+                                                             unsigned long long* unsorted)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned long long pairs = 0;
+    bool sorted = true;
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += stride) { // warp-uniform trips
         const int64_t j = b0 + threadIdx.x;
         int64_t lo = 0;
@@ -108,10 +110,12 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const in
         const bool is_long = j < n && len > kShortRow;
         if (j >= n || is_long)
             continue;
-        int32_t np = 0, cur_w = -1, maxw = -1;
+        int32_t np = 0, cur_w = -1, maxw = -1, prev_c = INT_MIN;
         uint32_t cur = 0;
         for (int32_t q = 0; q < len; ++q) {
             const int32_t c = __ldg(cols + lo + q);
+            sorted = sorted && c > prev_c;
+            prev_c = c;
             const int32_t w = c >> 5;
             const uint32_t bit = 1u << (c & 31);
             if (w == cur_w) {
@@ -149,10 +153,13 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const in
         pairs += __shfl_xor_sync(kFull, pairs, off);
     if ((threadIdx.x & 31) == 0 && pairs)
         atomicAdd(nnz_bc, pairs);
+    if (!__all_sync(kFull, sorted) && (threadIdx.x & 31) == 0)
+        atomicAdd(unsorted, 1ull);
 }
 
 __device__ __forceinline__ int compress_row_short(int64_t j, int64_t lo, int64_t len, int32_t col, int lane,
-                                                  int32_t* __restrict__ csize, int2* __restrict__ cp)
+                                                  int32_t* __restrict__ csize, int2* __restrict__ cp,
+                                                  bool* sorted_out)
 {
     const bool valid = lane < len;
     const int32_t w = col >> 5;
@@ -161,6 +168,9 @@ __device__ __forceinline__ int compress_row_short(int64_t j, int64_t lo, int64_t
     const uint32_t orv = group_or(grp, valid ? (1u << (col & 31)) : 0u, lane);
     const bool leader = valid && (__ffs(grp) - 1) == lane;
     const uint32_t lm = __ballot_sync(kFull, leader);
+    const int32_t prev = __shfl_up_sync(kFull, col, 1);
+    if (!__all_sync(kFull, !valid || lane == 0 || col > prev))
+        *sorted_out = false;
     if (leader)
         cp[lo + __popc(lm & lanemask_lt())] = make_int2(w, static_cast<int>(orv));
     if (lane == 0)
@@ -169,7 +179,7 @@ __device__ __forceinline__ int compress_row_short(int64_t j, int64_t lo, int64_t
 }
 
 __device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
-                                 int32_t* __restrict__ csize, int2* __restrict__ cp);
+                                 int32_t* __restrict__ csize, int2* __restrict__ cp, bool* sorted_out);
 
 // Warp kernel for rows of more than kShortRow entries.  A warp takes batches
 // of 32 consecutive rows: one coalesced load of their offsets, then the long
@@ -178,10 +188,12 @@ __device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32
 __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ cols,
                                                        int32_t* __restrict__ csize,
-                                                       int2* __restrict__ cp, unsigned long long* nnz_bc)
+                                                       int2* __restrict__ cp, unsigned long long* nnz_bc,
+                                                       unsigned long long* unsorted)
 {
     const int lane = threadIdx.x & 31;
     unsigned long long pairs = 0; // warp-uniform
+    bool sorted = true;           // warp-uniform
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < n; r0 += warps * 32) {
         const int64_t jr = r0 + lane;
@@ -205,9 +217,9 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
         };
         auto process = [&](int q, int64_t lo, int64_t len, int32_t col) {
             if (len <= 32)
-                pairs += compress_row_short(r0 + q, lo, len, col, lane, csize, cp);
+                pairs += compress_row_short(r0 + q, lo, len, col, lane, csize, cp, &sorted);
             else
-                pairs += compress_row_long(r0 + q, lo, len, cols, lane, csize, cp);
+                pairs += compress_row_long(r0 + q, lo, len, cols, lane, csize, cp, &sorted);
         };
         int64_t loA = 0, lenA = 0, loB = 0, lenB = 0;
         int32_t colA = 0, colB = 0;
@@ -229,10 +241,12 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t*
     }
     if (lane == 0 && pairs)
         atomicAdd(nnz_bc, pairs);
+    if (lane == 0 && !sorted)
+        atomicAdd(unsorted, 1ull);
 }
 
 __device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32_t* __restrict__ cols, int lane,
-                                 int32_t* __restrict__ csize, int2* __restrict__ cp)
+                                 int32_t* __restrict__ csize, int2* __restrict__ cp, bool* sorted_out)
 {
     {
         // long row: sortedness first (one extra read of the row, L1/L2 resident)
@@ -247,6 +261,8 @@ __device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32
             sorted = sorted && __all_sync(kFull, !valid || c > prev);
             prev_last = __shfl_sync(kFull, c, 31);
         }
+        if (!sorted)
+            *sorted_out = false;
         int32_t cnt = 0;
         if (sorted) {
             int32_t carry_w = -1;
@@ -1123,17 +1139,18 @@ cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, do
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
-                            int32_t* csize, int2* cp, unsigned long long* nnz_bc, cudaStream_t st)
+                            int32_t* csize, int2* cp, unsigned long long* nnz_bc, unsigned long long* unsorted,
+                            cudaStream_t st)
 {
     if (n <= 0)
         return cudaSuccess;
     // short rows: thread per row; longer rows: warp per row in batches of 32
     const int tblocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
-    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp, nnz_bc);
+    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp, nnz_bc, unsorted);
     count_launch();
     const int64_t batches = (n + 31) / 32;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((batches + 7) / 8, (int64_t)sm_count() * 8));
-    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp, nnz_bc);
+    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp, nnz_bc, unsorted);
     count_launch();
     return cudaGetLastError();
 }

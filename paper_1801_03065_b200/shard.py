@@ -126,3 +126,139 @@ def sharded_multiply(a, b, rank: int, world: int, group=None, cuts: Optional[lis
         allv = [mine]
     offs = block_offsets([int(t.item()) for t in allv])
     return Shard(rank, world, lo, hi, c, nnz_local, offs[rank], offs[-1], int(flops_local), handle)
+
+
+# ---------------------------------------------------------------------------
+# B distributed by rows: each rank owns a row block of B and receives only the
+# rows its block of A references (the stencil halo; with the
+# whole row range requested it is the all-gatherv fallback for a B that is
+# not replicated).
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class OwnedRows:
+    """Rows [lo, hi) of a CSR held by this rank: row offsets rebased to 0."""
+    lo: int
+    hi: int
+    row_offsets: object  # torch.int64 [hi-lo+1]
+    col_indices: object  # torch.int32
+    values: object       # torch.float64
+
+
+def own_rows(b, lo: int, hi: int) -> OwnedRows:
+    """This rank's row block of `b` (copied out of a full matrix; in a
+    distributed run it is what the rank holds to begin with)."""
+    ro = b.row_offsets[lo:hi + 1]
+    s, e = int(ro[0].item()), int(ro[-1].item())
+    return OwnedRows(lo, hi, (ro - s).clone(), b.col_indices[s:e].clone(), b.values[s:e].clone())
+
+
+def column_band(a, lo: int, hi: int) -> tuple:
+    """[r0, r1): the B rows that rows [lo, hi) of A reference, widened to
+    include [lo, hi) itself (for C = A*A the rank's own rows are its A block)."""
+    ro = a.row_offsets
+    s, e = int(ro[lo].item()), int(ro[hi].item())
+    if e <= s:
+        return (lo, hi)
+    cols = a.col_indices[s:e]
+    return (min(lo, int(cols.min().item())), max(hi, int(cols.max().item()) + 1))
+
+
+def _intersect(a0, a1, b0, b1):
+    lo, hi = max(a0, b0), min(a1, b1)
+    return (lo, hi) if hi > lo else None
+
+
+def exchange_band(own: OwnedRows, cuts: Sequence[int], need: tuple, rank: int, world: int,
+                  num_rows: int, num_cols: int, group=None, dist=None, needs: Optional[list] = None):
+    """Assemble this rank's view of B holding rows [need[0], need[1]).
+
+    Owners are given by `cuts` (rank q owns [cuts[q], cuts[q+1])).  Every
+    owner sends each requester the intersection of its rows with the
+    requested range: row lengths first, then columns and values (two rounds
+    of batched point-to-point transfers, NCCL on GPUs, gloo on CPU).  The
+    result is a DeviceCsr of num_rows rows whose row offsets are rebased so
+    that rows outside the band are empty; its columns are global.  Returns
+    (view, bytes received from other ranks)."""
+    import torch
+    if dist is None:
+        import torch.distributed as dist
+    from . import DeviceCsr
+    dev = own.row_offsets.device
+    if needs is None:
+        mine = torch.tensor([need[0], need[1]], dtype=torch.int64, device=dev)
+        allv = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(world)]
+        if world > 1:
+            dist.all_gather(allv, mine, group=group)
+        else:
+            allv = [mine]
+        needs = [tuple(int(x) for x in t.tolist()) for t in allv]
+    lens_own = own.row_offsets[1:] - own.row_offsets[:-1]
+
+    # round 1: row lengths of every piece
+    pieces = {}   # owner q -> (r0, r1) of the rows this rank receives from q
+    ops, recv_lens = [], {}
+    for q in range(world):
+        got = _intersect(cuts[q], cuts[q + 1], need[0], need[1])
+        if got is not None:
+            pieces[q] = got
+    for q in range(world):
+        if q == rank:
+            continue
+        give = _intersect(own.lo, own.hi, needs[q][0], needs[q][1])
+        if give is not None:
+            ops.append(dist.P2POp(dist.isend, lens_own[give[0] - own.lo:give[1] - own.lo].contiguous(), q,
+                                  group=group))
+        if q in pieces:
+            r0, r1 = pieces[q]
+            recv_lens[q] = torch.empty(r1 - r0, dtype=torch.int64, device=dev)
+            ops.append(dist.P2POp(dist.irecv, recv_lens[q], q, group=group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+    # round 2: columns and values
+    ops, recv = [], {}
+    nbytes = 0
+    for q in range(world):
+        if q == rank:
+            continue
+        give = _intersect(own.lo, own.hi, needs[q][0], needs[q][1])
+        if give is not None:
+            s = int(own.row_offsets[give[0] - own.lo].item())
+            e = int(own.row_offsets[give[1] - own.lo].item())
+            ops.append(dist.P2POp(dist.isend, own.col_indices[s:e].contiguous(), q, group=group))
+            ops.append(dist.P2POp(dist.isend, own.values[s:e].contiguous(), q, group=group))
+        if q in pieces:
+            n = int(recv_lens[q].sum().item())
+            ci = torch.empty(n, dtype=torch.int32, device=dev)
+            v = torch.empty(n, dtype=torch.float64, device=dev)
+            recv[q] = (ci, v)
+            ops.append(dist.P2POp(dist.irecv, ci, q, group=group))
+            ops.append(dist.P2POp(dist.irecv, v, q, group=group))
+            nbytes += recv_lens[q].numel() * 8 + n * 12
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+    # assemble in row order
+    lens, cols, vals = [], [], []
+    for q in sorted(pieces):
+        r0, r1 = pieces[q]
+        if q == rank:
+            s = int(own.row_offsets[r0 - own.lo].item())
+            e = int(own.row_offsets[r1 - own.lo].item())
+            lens.append(lens_own[r0 - own.lo:r1 - own.lo])
+            cols.append(own.col_indices[s:e])
+            vals.append(own.values[s:e])
+        else:
+            lens.append(recv_lens[q])
+            cols.append(recv[q][0])
+            vals.append(recv[q][1])
+    band_len = torch.cat(lens) if lens else torch.zeros(0, dtype=torch.int64, device=dev)
+    ro = torch.zeros(num_rows + 1, dtype=torch.int64, device=dev)
+    if band_len.numel():
+        ro[need[0] + 1:need[1] + 1] = torch.cumsum(band_len, 0)
+        ro[need[1] + 1:] = ro[need[1]]
+    ci = torch.cat(cols) if cols else torch.zeros(0, dtype=torch.int32, device=dev)
+    v = torch.cat(vals) if vals else torch.zeros(0, dtype=torch.float64, device=dev)
+    return DeviceCsr(num_rows, num_cols, ro, ci, v, True, int(ci.numel())), nbytes

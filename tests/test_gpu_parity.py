@@ -595,6 +595,83 @@ def test_heavy_rows_vs_oracle(kk, oracle):
     assert np.array_equal(sv.view(np.int64), gv.view(np.int64))
 
 
+def _sorted_parity(oracle, a, b, c):
+    ro = oracle.symbolic_row_offsets(a, b)
+    assert np.array_equal(c.row_offsets, ro)
+    cols, vals = oracle.numeric(a, b, ro)
+    sc, sv = oracle.sort_rows(ro, cols, vals)
+    gc, gv = oracle.sort_rows(ro, c.col_indices, c.values)
+    assert np.array_equal(sc, gc)
+    assert np.array_equal(sv.view(np.int64), gv.view(np.int64))
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_heavy_rows_column_slabs(kk, oracle, seed):
+    """Column-sorted B: heavy rows take the column-slab kernel (kk_slab.cu) —
+    adaptive slab widths, abandoned slabs, several A-entry groups per slab
+    (A rows longer than 256) — sorted columns identical, value bits equal."""
+    rng = np.random.default_rng(seed)
+    a = random_csr(rng, 40, 4000, 0.12)          # ~480 A entries per row: two run groups
+    b = random_csr(rng, 4000, 30000, 0.01 + 0.01 * (seed % 2))
+    h = kk.symbolic(a, b)
+    assert h.heavy_path == 2 and h.max_row_size > 1024
+    c = kk.numeric(a, b, h).to_host()
+    _sorted_parity(oracle, a, b, c)
+    # skewed columns (dense low columns, sparse tail): slab widths adapt
+    cols = np.minimum((rng.pareto(1.2, size=b.nnz()) * 300).astype(np.int64), 29999).astype(np.int32)
+    bs = []
+    for i in range(b.num_rows):
+        lo, hi = b.row_offsets[i], b.row_offsets[i + 1]
+        bs.append(np.unique(cols[lo:hi]))
+    ro = np.zeros(b.num_rows + 1, np.int64)
+    np.cumsum([len(x) for x in bs], out=ro[1:])
+    b2 = kk.CsrMatrix(b.num_rows, b.num_cols, ro, np.concatenate(bs).astype(np.int32),
+                      rng.uniform(-1, 1, int(ro[-1])), True)
+    res = kk.multiply(a, b2)
+    assert res.handle.heavy_path == 2
+    _sorted_parity(oracle, a, b2, res.c.to_host())
+
+
+def test_heavy_row_beyond_half_a_million_outputs(kk, oracle):
+    """A row of 600,000 outputs stays on a CTA path (no row-size cliff)."""
+    rng = np.random.default_rng(17)
+    nb, per, k = 600, 1000, 600_000
+    cols = np.concatenate([np.sort(rng.choice(k, per, replace=False)) for _ in range(nb)])
+    cols[:k] = np.arange(k)  # the first 600 rows tile every column once
+    rows = []
+    for i in range(nb):
+        rows.append(np.sort(cols[i * per:(i + 1) * per]))
+    bro = np.arange(nb + 1, dtype=np.int64) * per
+    b = kk.CsrMatrix(nb, k, bro, np.concatenate(rows).astype(np.int32), rng.uniform(-1, 1, nb * per), True)
+    a = kk.CsrMatrix(2, nb, np.array([0, nb, nb + 7], np.int64),
+                     np.concatenate([np.arange(nb), np.arange(7)]).astype(np.int32), rng.uniform(-1, 1, nb + 7), True)
+    res = kk.multiply(a, b)
+    h = res.handle
+    assert h.max_row_size == k and h.heavy_path == 2
+    _sorted_parity(oracle, a, b, res.c.to_host())
+
+
+def test_heavy_rows_unsorted_b(kk, oracle):
+    """Unsorted B rows: the hashed-bucket heavy kernel; reusing a slab plan
+    with an unsorted B of the same structure size raises instead of
+    returning a wrong C."""
+    rng = np.random.default_rng(19)
+    a = random_csr(rng, 24, 3000, 0.08)
+    b = random_csr(rng, 3000, 20000, 0.02)
+    bu = random_csr(rng, 3000, 20000, 0.02, shuffle=True)
+    res = kk.multiply(a, bu)
+    assert res.handle.heavy_path == 1
+    _sorted_parity(oracle, a, bu, res.c.to_host())
+    h = kk.symbolic(a, b)
+    assert h.heavy_path == 2
+    perm = kk.CsrMatrix(b.num_rows, b.num_cols, b.row_offsets, b.col_indices.copy(), b.values, False)
+    for i in range(b.num_rows):
+        lo, hi = perm.row_offsets[i], perm.row_offsets[i + 1]
+        perm.col_indices[lo:hi] = perm.col_indices[lo:hi][::-1]
+    with pytest.raises(kk.InternalError, match="sorted"):
+        kk.numeric(a, perm, h, kk.PhaseStats())
+
+
 def test_row_flops_kernel(kk, oracle):
     from paper_1801_03065_b200 import generators as G
     a = G.rmat(12, 16, 1)

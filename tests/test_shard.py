@@ -104,3 +104,63 @@ def test_gloo_world2_sharded_multiply(tmp_path, oracle):
     assert total == fl
     # flop balance: the two halves differ by at most one row's flops
     assert abs(int(blocks[0]["fl"]) - int(blocks[1]["fl"])) <= 729
+
+
+def _band_worker(rank, world, port, outdir, kind):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1801_03065_b200 as kk
+    from paper_1801_03065_b200 import generators as G
+    from oracle.oracle import Oracle
+    a = G.laplace3d(9) if kind == "stencil" else G.rmat(8, 8, 3)
+    da = kk.DeviceCsr(a.num_rows, a.num_cols, torch.from_numpy(a.row_offsets), torch.from_numpy(a.col_indices),
+                      torch.from_numpy(a.values), True, a.nnz())
+    per_row, _, _ = Oracle().flops_stats(a, a)
+    cuts = shard.flop_cut_points(np.cumsum(per_row), world)
+    lo, hi = cuts[rank], cuts[rank + 1]
+    own = shard.own_rows(da, lo, hi)  # the only rows of B = A this rank holds
+    out = {}
+    for mode in ("band", "all"):
+        need = shard.column_band(da, lo, hi) if mode == "band" else (0, a.num_rows)
+        band, nbytes = shard.exchange_band(own, cuts, need, rank, world, a.num_rows, a.num_cols)
+        s = shard.sharded_multiply(band, band, rank, world, cuts=cuts, compute=_cpu_compute)
+        out[mode] = dict(lo=s.lo, hi=s.hi, base=s.base, ro=s.c.row_offsets.numpy(), ci=s.c.col_indices.numpy(),
+                         v=s.c.values.numpy(), need0=need[0], need1=need[1], nbytes=nbytes,
+                         band_nnz=band.nnz())
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), **{f"{m}_{k}": v for m, d in out.items() for k, v in d.items()})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind", [(2, "stencil"), (3, "stencil"), (3, "rmat")])
+def test_gloo_band_exchange(tmp_path, oracle, world, kind):
+    """B distributed by row blocks (each rank holds only its own rows of B = A):
+    the band exchange delivers exactly the rows a block references — the halo
+    for a stencil — and with the whole range requested it is an all-gatherv.
+    The assembled C blocks equal the single-process product bit for bit."""
+    mp.spawn(_band_worker, args=(world, _free_port(), str(tmp_path), kind), nprocs=world, join=True)
+    from paper_1801_03065_b200 import generators as G
+    a = G.laplace3d(9) if kind == "stencil" else G.rmat(8, 8, 3)
+    ro, cols, vals = oracle.multiply(a, a)
+    blocks = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
+    for mode in ("band", "all"):
+        for b in blocks:
+            lo, hi, base = int(b[f"{mode}_lo"]), int(b[f"{mode}_hi"]), int(b[f"{mode}_base"])
+            assert base == ro[lo]
+            assert np.array_equal(b[f"{mode}_ro"] + base, ro[lo:hi + 1])
+            assert np.array_equal(b[f"{mode}_ci"], cols[ro[lo]:ro[hi]])
+            assert np.array_equal(b[f"{mode}_v"].view(np.int64), vals[ro[lo]:ro[hi]].view(np.int64))
+    if kind == "stencil":
+        n = 9
+        halo = n * n + n + 1
+        for r, b in enumerate(blocks):
+            lo, hi = int(b["band_lo"]), int(b["band_hi"])
+            # the band of a 27-point stencil block is at most the block plus one
+            # plane, one line and one point on each side
+            assert max(0, lo - halo) <= int(b["band_need0"]) <= lo
+            assert hi <= int(b["band_need1"]) <= min(n ** 3, hi + halo)
+            assert int(b["all_band_nnz"]) == a.nnz()
+            assert 0 < int(b["band_nbytes"]) < int(b["all_nbytes"])
