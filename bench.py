@@ -809,7 +809,12 @@ def run_sharded(args, kk, shard, mats, dev, timer, barrier, rank, world, dist):
     bc_bytes = A.row_offsets.numel() * 8 + a_host.nnz() * 12
 
     # band exchange: each rank owns its rows of B (= its rows of A) and
-    # receives the rows its block references from their owners
+    # receives the rows its block references from their owners (point-to-point
+    # transfers: NCCL only; the gloo smoke path skips it)
+    res_band = None
+    if os.environ.get("KK_BENCH_BACKEND", "nccl") != "nccl":
+        return _sharded_result(args, a_host, info, lo, hi, ms_total, ms_num, launches, clk, ms_bc, bc_bytes, rank,
+                               None, kk, dev, barrier, timer, nnz_c, flops)
     own = shard.own_rows(A, lo, hi)
     need = shard.column_band(A, lo, hi)
 
@@ -823,6 +828,12 @@ def run_sharded(args, kk, shard, mats, dev, timer, barrier, rank, world, dist):
     barrier()
     ms_band = timer.run(step_band, args.steps)
     barrier()
+    return _sharded_result(args, a_host, info, lo, hi, ms_total, ms_num, launches, clk, ms_bc, bc_bytes, rank,
+                           (ms_band, getattr(step_band, "bytes", 0)), kk, dev, barrier, timer, nnz_c, flops)
+
+
+def _sharded_result(args, a_host, info, lo, hi, ms_total, ms_num, launches, clk, ms_bc, bc_bytes, rank, band, kk,
+                    dev, barrier, timer, nnz_c, flops):
     m = hi - lo
     res = {
         "ms_total": ms_total, "flops": flops, "nnz_c": nnz_c, "m": m, "nnz_a": a_host.nnz(),
@@ -833,10 +844,12 @@ def run_sharded(args, kk, shard, mats, dev, timer, barrier, rank, world, dist):
                          "path": "numeric on the rank's row block, B resident"},
         "with_broadcast": {"ms_total": ms_bc, "bytes": bc_bytes if rank == 0 else 0,
                            "path": "full B broadcast from rank 0 over NCCL each step, then the sharded multiply"},
-        "with_band_exchange": {"ms_total": ms_band, "bytes": getattr(step_band, "bytes", 0),
-                               "path": "each rank owns its rows of B = A and receives the rows its block "
-                                       "references (stencil halo) from their owners (NCCL P2P), then multiplies"},
     }
+    if band is not None:
+        res["with_band_exchange"] = {
+            "ms_total": band[0], "bytes": band[1],
+            "path": "each rank owns its rows of B = A and receives the rows its block references (stencil halo) "
+                    "from their owners (NCCL P2P), then multiplies"}
     if not args.no_e2e:
         res["e2e"] = e2e_multiply_host(args, kk, a_host, nnz_c, dev, barrier, stream=timer.stream, a_rows=(lo, hi))
     return res

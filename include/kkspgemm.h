@@ -145,7 +145,9 @@ typedef struct spg_handle* spg_handle_t;
 
 /* Host-side description used to rebuild a device handle from the fields of a
  * reference SpgemmHandle (the engine.hpp shim path).  c_row_offsets is HOST
- * memory [m+1]. */
+ * memory [m+1].  A handle whose config.accumulator is Auto and whose
+ * numeric_choice is what resolve_config yields keeps the GPU's own numeric
+ * plan (fast kernels, slot replay); an edited choice is honoured as forced. */
 typedef struct spg_handle_desc {
     int32_t m, n, k;
     int64_t nnz_a, nnz_b;
@@ -160,6 +162,8 @@ typedef struct spg_handle_desc {
     spg_config config;
     spg_phase_stats symbolic_stats;
     double compress_ms;
+    const int64_t* per_row_flops;   /* HOST [m] (FlopsStats::per_row_flops) or NULL:
+                                       enables the heavy-row order and the slot replay */
 } spg_handle_desc;
 
 /* Last error message of the calling thread ("" after success). */
@@ -228,6 +232,16 @@ int spg_sort_rows(int32_t m, const int64_t* d_row_offsets, int32_t* d_cols, doub
  * multigrid triple product.  Synchronises once (the longest result row). */
 int spg_transpose(const spg_csr* a, int64_t* d_t_row_offsets, int32_t* d_t_cols, double* d_t_vals,
                   void* stream);
+
+/* Per-row canonical digests of a device CSR (extension; the device side of
+ * the reference's canonicalize + compare_canonical, oracle.cpp:105-159):
+ * d_out[i] = sum over the row's entries of mix(column, value bits) plus
+ * mix(row length), mix the splitmix64 finalizer — independent of the column
+ * order, so it is the digest of the sorted row.  The oracle computes the same
+ * function on the CPU; equal digests mean equal sorted columns and bitwise
+ * equal values.  Stream-ordered. */
+int spg_row_digests(int32_t m, const int64_t* d_row_offsets, const int32_t* d_cols, const double* d_vals,
+                    uint64_t* d_out, void* stream);
 
 /* Per-row multiplication counts (flops_stats per_row_flops, csr_matrix.cpp:136-154)
  * into device memory d_out[a->num_rows]; stream-ordered.  Used for the

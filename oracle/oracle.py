@@ -48,6 +48,8 @@ class Oracle:
             "orc_sort_rows": [C.c_int32, _P, _P, _P],
             "orc_resolve_config": [C.c_int, C.c_int32, C.c_double, C.c_int, C.c_int, C.c_int,
                                    C.c_int32, C.c_int32, C.c_double, C.c_int64, _P],
+            "orc_row_digests": [C.c_int32, _P, _P, _P, _P],
+            "orc_product_row_digests": [C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_int, _P, _P],
         }.items():
             getattr(L, f).restype = C.c_int
             getattr(L, f).argtypes = args
@@ -118,6 +120,26 @@ class Oracle:
         ro = np.ascontiguousarray(rowptr, np.int64) - int(rowptr[0])
         self.L.orc_sort_rows(len(ro) - 1, _ptr(ro), _ptr(cols), _ptr(vals))
         return cols, vals
+
+    def row_digests(self, m):
+        """Per-row canonical digests of a CSR (order-independent; see spgemm_oracle.h)."""
+        ro, ci, v = self._norm(m)
+        out = np.empty(max(m.num_rows, 1), np.uint64)
+        self.L.orc_row_digests(m.num_rows, _ptr(ro), _ptr(ci), _ptr(v), _ptr(out))
+        return out[:m.num_rows]
+
+    def product_row_digests(self, a, b, threads=None):
+        """(digests, row sizes) of every row of C = A*B, formed by the numeric
+        restatement in `threads` threads without storing C."""
+        ar, ac, av = self._norm(a)
+        br, bc, bv = self._norm(b)
+        out = np.empty(max(a.num_rows, 1), np.uint64)
+        sizes = np.empty(max(a.num_rows, 1), np.int64)
+        rc = self.L.orc_product_row_digests(a.num_rows, b.num_cols, _ptr(ar), _ptr(ac), _ptr(av), _ptr(br),
+                                            _ptr(bc), _ptr(bv), int(threads or os.cpu_count() or 1), _ptr(out),
+                                            _ptr(sizes))
+        assert rc == 0
+        return out[:a.num_rows], sizes[:a.num_rows]
 
     def max_rel_error(self, expected, actual):
         e = np.ascontiguousarray(expected, np.float64)

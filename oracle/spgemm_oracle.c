@@ -246,3 +246,130 @@ int orc_resolve_config(int phase, int32_t k, double avg_row_flops, int applied,
     out->l1_capacity = cfg_l1_capacity > 0 ? cfg_l1_capacity : out->l2_capacity;
     return 0;
 }
+
+/* ---- per-row canonical digests (test infrastructure) ---------------------
+ * The canonical form of a row (src/oracle.cpp:105-120 sorts each row by
+ * column) summarised as an ORDER-INDEPENDENT 64-bit digest: the sum of a
+ * mixed hash of every (column, value bits) pair plus a hash of the row
+ * length, so any column order gives the digest of the sorted row.  Equal
+ * digests <=> equal sorted columns and bitwise-equal values (up to 2^-64).
+ * libkkspgemm.so computes the same function on the device (spg_row_digests).
+ * The product C is formed row by row with the numeric restatement above (dense
+ * accumulator, left-to-right sums) and never stored, in nthreads threads. */
+#include <pthread.h>
+
+static uint64_t orc_mix64(uint64_t x)
+{
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+static uint64_t orc_entry_hash(int32_t col, double v)
+{
+    uint64_t bits;
+    memcpy(&bits, &v, sizeof(bits));
+    return orc_mix64(((uint64_t)(uint32_t)col * 0x9E3779B97F4A7C15ull) ^ orc_mix64(bits));
+}
+
+int orc_row_digests(int32_t m, const int64_t* rowptr, const int32_t* cols, const double* vals, uint64_t* out)
+{
+    for (int32_t i = 0; i < m; ++i) {
+        uint64_t d = orc_mix64((uint64_t)(rowptr[i + 1] - rowptr[i]) + 0x2545F4914F6CDD1Dull);
+        for (int64_t q = rowptr[i]; q < rowptr[i + 1]; ++q)
+            d += orc_entry_hash(cols[q], vals[q]);
+        out[i] = d;
+    }
+    return 0;
+}
+
+typedef struct {
+    int32_t m, k;
+    const int64_t *a_rowptr, *b_rowptr;
+    const int32_t *a_cols, *b_cols;
+    const double *a_vals, *b_vals;
+    uint64_t* out;
+    int64_t* sizes;
+    int32_t next;
+    pthread_mutex_t mu;
+} digest_job;
+
+static void* digest_worker(void* arg)
+{
+    digest_job* J = (digest_job*)arg;
+    double* acc = (double*)malloc(sizeof(double) * (size_t)(J->k > 0 ? J->k : 1));
+    int32_t* seen = (int32_t*)malloc(sizeof(int32_t) * (size_t)(J->k > 0 ? J->k : 1));
+    int32_t* touched = (int32_t*)malloc(sizeof(int32_t) * (size_t)(J->k > 0 ? J->k : 1));
+    if (!acc || !seen || !touched) {
+        free(acc);
+        free(seen);
+        free(touched);
+        return (void*)1;
+    }
+    for (int32_t c = 0; c < J->k; ++c)
+        seen[c] = -1;
+    for (;;) {
+        pthread_mutex_lock(&J->mu);
+        const int32_t i0 = J->next;
+        J->next = i0 + 256 < J->m ? i0 + 256 : J->m;
+        pthread_mutex_unlock(&J->mu);
+        if (i0 >= J->m)
+            break;
+        const int32_t i1 = i0 + 256 < J->m ? i0 + 256 : J->m;
+        for (int32_t i = i0; i < i1; ++i) {
+            int64_t used = 0;
+            for (int64_t p = J->a_rowptr[i]; p < J->a_rowptr[i + 1]; ++p) {
+                const int32_t j = J->a_cols[p];
+                const double av = J->a_vals[p];
+                for (int64_t q = J->b_rowptr[j]; q < J->b_rowptr[j + 1]; ++q) {
+                    const int32_t c = J->b_cols[q];
+                    const double prod = av * J->b_vals[q];
+                    if (seen[c] != i) { /* first touch: the sum starts at the first product */
+                        seen[c] = i;
+                        acc[c] = prod;
+                        touched[used++] = c;
+                    } else {
+                        acc[c] += prod;
+                    }
+                }
+            }
+            uint64_t d = orc_mix64((uint64_t)used + 0x2545F4914F6CDD1Dull);
+            for (int64_t t = 0; t < used; ++t)
+                d += orc_entry_hash(touched[t], acc[touched[t]]);
+            J->out[i] = d;
+            if (J->sizes)
+                J->sizes[i] = used;
+        }
+    }
+    free(acc);
+    free(seen);
+    free(touched);
+    return NULL;
+}
+
+int orc_product_row_digests(int32_t m, int32_t k, const int64_t* a_rowptr, const int32_t* a_cols,
+                            const double* a_vals, const int64_t* b_rowptr, const int32_t* b_cols,
+                            const double* b_vals, int nthreads, uint64_t* out, int64_t* sizes)
+{
+    digest_job J = {m, k, a_rowptr, b_rowptr, a_cols, b_cols, a_vals, b_vals, out, sizes, 0};
+    pthread_mutex_init(&J.mu, NULL);
+    if (nthreads < 1)
+        nthreads = 1;
+    if (nthreads > 256)
+        nthreads = 256;
+    pthread_t th[256];
+    int rc = 0;
+    for (int t = 0; t < nthreads; ++t)
+        pthread_create(&th[t], NULL, digest_worker, &J);
+    for (int t = 0; t < nthreads; ++t) {
+        void* r = NULL;
+        pthread_join(th[t], &r);
+        if (r)
+            rc = 1;
+    }
+    pthread_mutex_destroy(&J.mu);
+    return rc;
+}

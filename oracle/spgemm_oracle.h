@@ -72,6 +72,18 @@ int orc_resolve_config(int phase, int32_t k, double avg_row_flops, int applied,
                        int32_t dense_cutoff_k, double avg_flops_cutoff,
                        int64_t row_upper_bound, orc_resolved* out);
 
+/* Per-row canonical digests: an order-independent 64-bit hash of each row's
+ * (column, value bits) set and its length, the digest of the row sorted as
+ * canonicalize does (src/oracle.cpp:105-120).  orc_row_digests digests a
+ * given CSR; orc_product_row_digests forms each row of C = A*B with the
+ * numeric restatement (left-to-right sums from the first product) in
+ * nthreads threads and digests it without storing C (sizes[i] = row size,
+ * may be NULL).  libkkspgemm.so's spg_row_digests is the device twin. */
+int orc_row_digests(int32_t m, const int64_t* rowptr, const int32_t* cols, const double* vals, uint64_t* out);
+int orc_product_row_digests(int32_t m, int32_t k, const int64_t* a_rowptr, const int32_t* a_cols,
+                            const double* a_vals, const int64_t* b_rowptr, const int32_t* b_cols,
+                            const double* b_vals, int nthreads, uint64_t* out, int64_t* sizes);
+
 #ifdef __cplusplus
 }
 #endif

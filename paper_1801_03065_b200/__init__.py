@@ -150,7 +150,8 @@ class _Desc(C.Structure):
                 ("flops", _Flops), ("compression", _Report), ("max_row_size", C.c_int64),
                 ("avg_row_size", C.c_double), ("avg_row_size_estimate", C.c_double),
                 ("symbolic_choice", _Resolved), ("numeric_choice", _Resolved),
-                ("config", _Config), ("symbolic_stats", _PhaseStats), ("compress_ms", C.c_double)]
+                ("config", _Config), ("symbolic_stats", _PhaseStats), ("compress_ms", C.c_double),
+                ("per_row_flops", C.c_void_p)]
 
 
 # every symbol include/kkspgemm.h declares (checked by tests/test_abi.py)
@@ -158,7 +159,7 @@ EXPORTED_SYMBOLS = (
     "spg_last_error", "spg_config_init", "spg_resolve_config", "spg_flat_position",
     "spg_symbolic", "spg_numeric", "spg_handle_info_get", "spg_handle_copy_row_offsets",
     "spg_handle_copy_per_row_flops", "spg_handle_copy_row_offsets_device", "spg_handle_set_numeric", "spg_handle_import",
-    "spg_handle_check", "spg_handle_destroy", "spg_sort_rows", "spg_kernel_launch_count",
+    "spg_handle_check", "spg_handle_destroy", "spg_sort_rows", "spg_kernel_launch_count", "spg_row_digests",
     "spg_row_flops", "spg_handle_replay_state", "spg_numeric_rows", "spg_transpose",
 )
 
@@ -206,6 +207,8 @@ def lib() -> C.CDLL:
                                         C.POINTER(C.c_int64)]
         L.spg_sort_rows.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.spg_row_flops.argtypes = [C.POINTER(_Csr), C.POINTER(_Csr), C.c_void_p, C.c_void_p]
+        L.spg_row_digests.restype = C.c_int
+        L.spg_row_digests.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib_handle = L
     return _lib_handle
 
@@ -615,6 +618,18 @@ def transpose(a, stream=None) -> DeviceCsr:
     v = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
     _check(lib().spg_transpose(C.byref(da._c()), ro.data_ptr(), ci.data_ptr(), v.data_ptr(), _stream_ptr(stream)))
     return DeviceCsr(da.num_cols, da.num_rows, ro, ci[:nnz], v[:nnz], True, nnz)
+
+
+def row_digests(c: DeviceCsr, stream=None):
+    """Per-row canonical digests of a device CSR (torch.int64 [m] holding the
+    uint64 bits): order-independent hash of each row's (column, value bits)
+    set and length — the device side of canonicalize + compare_canonical
+    (oracle.cpp:105-159); the oracle computes the same function."""
+    import torch
+    out = torch.empty(max(c.num_rows, 1), dtype=torch.int64, device=c.row_offsets.device)
+    _check(lib().spg_row_digests(c.num_rows, c.row_offsets.data_ptr(), c.col_indices.data_ptr(),
+                                 c.values.data_ptr(), out.data_ptr(), _stream_ptr(stream)))
+    return out[:c.num_rows]
 
 
 def sort_rows(c: DeviceCsr, stream=None) -> DeviceCsr:

@@ -5,15 +5,28 @@
 // every other reference TU and every caller (cli.cpp bench/verify, the unit
 // and acceptance tests) builds unchanged against the same header.
 //
-// Host CsrMatrix operands are copied to the device per call, the device
-// handle is rebuilt from the host SpgemmHandle fields on every numeric()
-// (so handle copies and edits of handle.config/numeric_choice behave exactly
-// as in the reference, acceptance_main.cpp:417-425), and C is copied back into
-// owning host vectors.  The device-resident fast path (no copies) is the C ABI
-// itself, which bench.py times.
+// The host SpgemmHandle stays the source of truth (handle copies and edits of
+// handle.config / numeric_choice behave exactly as in the reference,
+// acceptance_main.cpp:417-425).  Behind it, a small cache keeps the DEVICE
+// handle and device operand buffers of recently used handles, keyed by the
+// identity of the handle's c_row_offsets buffer and checked against a digest
+// of every field the device plan depends on (row offsets included), so
+//   * multiply() = symbolic() + numeric() uploads the operands once and runs
+//     the numeric on the device handle symbolic() built;
+//   * repeated numeric() on one handle (structure reuse) reaches the GPU's
+//     slot replay from the third pass on;
+//   * an Auto handle imported from host fields keeps the GPU's own plan.
+// Operands and C travel through one pinned staging pair with the copies split
+// into chunks that overlap (async H2D/D2H on one stream while the host copies
+// the next chunk).
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -48,36 +61,118 @@ void cuda(cudaError_t e)
         throw SpgemmError(std::string("CUDA: ") + cudaGetErrorString(e));
 }
 
+// pinned staging: host vectors are pageable, so copies go through a pinned
+// bounce buffer in chunks, the host memcpy of chunk i+1 overlapping the DMA
+// of chunk i
+struct Staging {
+    static constexpr size_t kChunk = size_t{32} << 20;
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    Staging()
+    {
+        for (int q = 0; q < 2; ++q) {
+            cuda(cudaHostAlloc(&buf[q], kChunk, cudaHostAllocPortable));
+            cuda(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
+        }
+    }
+    ~Staging()
+    {
+        for (int q = 0; q < 2; ++q) {
+            if (done[q])
+                cudaEventDestroy(done[q]);
+            if (buf[q])
+                cudaFreeHost(buf[q]);
+        }
+    }
+    Staging(const Staging&) = delete;
+    Staging& operator=(const Staging&) = delete;
+
+    void up(void* dst, const void* src, size_t bytes, cudaStream_t st)
+    {
+        const char* s = static_cast<const char*>(src);
+        char* d = static_cast<char*>(dst);
+        for (size_t off = 0, q = 0; off < bytes; off += kChunk, q ^= 1) {
+            const size_t n = bytes - off < kChunk ? bytes - off : kChunk;
+            cuda(cudaEventSynchronize(done[q])); // the buffer's previous DMA has drained
+            std::memcpy(buf[q], s + off, n);
+            cuda(cudaMemcpyAsync(d + off, buf[q], n, cudaMemcpyHostToDevice, st));
+            cuda(cudaEventRecord(done[q], st));
+        }
+    }
+
+    void down(void* dst, const void* src, size_t bytes, cudaStream_t st)
+    {
+        const char* s = static_cast<const char*>(src);
+        char* d = static_cast<char*>(dst);
+        size_t pend_off[2] = {0, 0}, pend_n[2] = {0, 0};
+        auto drain = [&](int q) {
+            if (pend_n[q]) {
+                cuda(cudaEventSynchronize(done[q]));
+                std::memcpy(d + pend_off[q], buf[q], pend_n[q]);
+                pend_n[q] = 0;
+            }
+        };
+        int q = 0;
+        for (size_t off = 0; off < bytes; off += kChunk, q ^= 1) {
+            const size_t n = bytes - off < kChunk ? bytes - off : kChunk;
+            drain(q);
+            cuda(cudaMemcpyAsync(buf[q], s + off, n, cudaMemcpyDeviceToHost, st));
+            cuda(cudaEventRecord(done[q], st));
+            pend_off[q] = off;
+            pend_n[q] = n;
+        }
+        drain(q);
+        drain(q ^ 1);
+    }
+};
+
+// device copy of one host CSR (buffers grow, never shrink)
 struct DevCsr {
     int64_t* ro = nullptr;
     int32_t* ci = nullptr;
     double* v = nullptr;
+    size_t cap_rows = 0, cap_nnz = 0;
     spg_csr view{};
-    explicit DevCsr(const CsrMatrix& m)
-    {
-        const int64_t nnz = m.nnz();
-        cuda(cudaMalloc(&ro, sizeof(int64_t) * (static_cast<size_t>(m.num_rows) + 1)));
-        cuda(cudaMalloc(&ci, sizeof(int32_t) * static_cast<size_t>(nnz > 0 ? nnz : 1)));
-        cuda(cudaMalloc(&v, sizeof(double) * static_cast<size_t>(nnz > 0 ? nnz : 1)));
-        if (m.row_offsets.empty())
-            cuda(cudaMemset(ro, 0, sizeof(int64_t)));
-        else
-            cuda(cudaMemcpy(ro, m.row_offsets.data(), sizeof(int64_t) * m.row_offsets.size(),
-                            cudaMemcpyHostToDevice));
-        if (nnz > 0) {
-            cuda(cudaMemcpy(ci, m.col_indices.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
-            cuda(cudaMemcpy(v, m.values.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice));
-        }
-        view = spg_csr{m.num_rows, m.num_cols, nnz, ro, ci, v};
-    }
+    DevCsr() = default;
+    DevCsr(const DevCsr&) = delete;
+    DevCsr& operator=(const DevCsr&) = delete;
     ~DevCsr()
     {
         cudaFree(ro);
         cudaFree(ci);
         cudaFree(v);
     }
-    DevCsr(const DevCsr&) = delete;
-    DevCsr& operator=(const DevCsr&) = delete;
+    void upload(const CsrMatrix& m, Staging& stg, cudaStream_t st, bool values_only)
+    {
+        const int64_t nnz = m.nnz();
+        const size_t rows = static_cast<size_t>(m.num_rows) + 1;
+        const size_t n = static_cast<size_t>(nnz > 0 ? nnz : 1);
+        if (rows > cap_rows) {
+            cudaFree(ro);
+            cuda(cudaMalloc(&ro, sizeof(int64_t) * rows));
+            cap_rows = rows;
+            values_only = false;
+        }
+        if (n > cap_nnz) {
+            cudaFree(ci);
+            cudaFree(v);
+            cuda(cudaMalloc(&ci, sizeof(int32_t) * n));
+            cuda(cudaMalloc(&v, sizeof(double) * n));
+            cap_nnz = n;
+            values_only = false;
+        }
+        if (!values_only) {
+            if (m.row_offsets.empty())
+                cuda(cudaMemsetAsync(ro, 0, sizeof(int64_t), st));
+            else
+                stg.up(ro, m.row_offsets.data(), sizeof(int64_t) * m.row_offsets.size(), st);
+            if (nnz > 0)
+                stg.up(ci, m.col_indices.data(), sizeof(int32_t) * nnz, st);
+        }
+        if (nnz > 0)
+            stg.up(v, m.values.data(), sizeof(double) * nnz, st);
+        view = spg_csr{m.num_rows, m.num_cols, nnz, ro, ci, v};
+    }
 };
 
 spg_config to_c(const SpgemmConfig& c)
@@ -133,6 +228,160 @@ struct HandleGuard {
     ~HandleGuard() { spg_handle_destroy(h); }
 };
 
+// ---- device-handle cache ------------------------------------------------------
+uint64_t mix(uint64_t h, uint64_t x)
+{
+    h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    return h;
+}
+
+uint64_t bytes_digest(uint64_t h, const void* p, size_t n)
+{
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    size_t q = 0;
+    for (; q + 8 <= n; q += 8) {
+        uint64_t x;
+        std::memcpy(&x, b + q, 8);
+        h = mix(h, x);
+    }
+    for (; q < n; ++q)
+        h = mix(h, b[q]);
+    return h;
+}
+
+// every host field the device plan depends on
+uint64_t handle_digest(const SpgemmHandle& h)
+{
+    uint64_t d = 0x6B6B7370;
+    for (int64_t x : {int64_t{h.m}, int64_t{h.n}, int64_t{h.k}, h.nnz_a, h.nnz_b, h.max_row_size})
+        d = mix(d, static_cast<uint64_t>(x));
+    const spg_config c = to_c(h.config);
+    const spg_resolved r = to_c(h.numeric_choice);
+    d = bytes_digest(d, &c, sizeof(c));
+    d = bytes_digest(d, &r, sizeof(r));
+    return bytes_digest(d, h.c_row_offsets.data(), sizeof(int64_t) * h.c_row_offsets.size());
+}
+
+struct Entry {
+    const void* key = nullptr;   // the host handle's c_row_offsets buffer
+    uint64_t digest = 0;
+    spg_handle_t h = nullptr;
+    DevCsr a, b;
+    bool b_is_a = false;
+    const CsrMatrix* fresh_a = nullptr; // operands symbolic() just uploaded
+    const CsrMatrix* fresh_b = nullptr;
+    int32_t* dc = nullptr;
+    double* dv = nullptr;
+    size_t cap_c = 0;
+    Staging* stg = nullptr; // the cache's (used under its mutex)
+    uint64_t last_use = 0;
+    Entry() = default;
+    Entry(const Entry&) = delete;
+    Entry& operator=(const Entry&) = delete;
+    ~Entry()
+    {
+        spg_handle_destroy(h);
+        cudaFree(dc);
+        cudaFree(dv);
+    }
+    const spg_csr* bview() const { return b_is_a ? &a.view : &b.view; }
+    void upload(const CsrMatrix& x, const CsrMatrix& y)
+    {
+        a.upload(x, *stg, nullptr, false);
+        b_is_a = &x == &y;
+        if (!b_is_a)
+            b.upload(y, *stg, nullptr, false);
+    }
+};
+
+class Cache {
+public:
+    static Cache& get()
+    {
+        static Cache c;
+        return c;
+    }
+    std::mutex mu;
+    // one pinned staging pair for every transfer (pinned allocation is slow
+    // and synchronises the device: never per call)
+    Staging& staging()
+    {
+        if (!stg)
+            stg = std::make_unique<Staging>();
+        return *stg;
+    }
+    // a few entries: every one holds the operands and C on the device
+    size_t capacity() const
+    {
+        const char* e = std::getenv("KK_SHIM_CACHE");
+        return e ? static_cast<size_t>(std::max(0, std::atoi(e))) : 2;
+    }
+    Entry* find(const void* key, uint64_t digest)
+    {
+        for (auto& e : entries)
+            if (e->key == key && e->digest == digest) {
+                e->last_use = ++clock;
+                return e.get();
+            }
+        return nullptr;
+    }
+    Entry* insert(std::unique_ptr<Entry> e)
+    {
+        for (auto it = entries.begin(); it != entries.end();)
+            if ((*it)->key == e->key)
+                it = entries.erase(it); // a stale entry of the same buffer
+            else
+                ++it;
+        const size_t cap = capacity();
+        if (cap == 0) {
+            scratch = std::move(e);
+            return scratch.get();
+        }
+        while (entries.size() >= cap) {
+            auto lru = std::min_element(entries.begin(), entries.end(),
+                                        [](const auto& x, const auto& y) { return x->last_use < y->last_use; });
+            entries.erase(lru);
+        }
+        e->last_use = ++clock;
+        entries.push_back(std::move(e));
+        return entries.back().get();
+    }
+
+private:
+    std::unique_ptr<Staging> stg;
+    std::vector<std::unique_ptr<Entry>> entries;
+    std::unique_ptr<Entry> scratch; // the uncached entry of the last call (KK_SHIM_CACHE=0)
+    uint64_t clock = 0;
+};
+
+std::unique_ptr<Entry> import_entry(const SpgemmHandle& handle)
+{
+    spg_handle_desc d{};
+    d.m = handle.m;
+    d.n = handle.n;
+    d.k = handle.k;
+    d.nnz_a = handle.nnz_a;
+    d.nnz_b = handle.nnz_b;
+    d.c_row_offsets = handle.c_row_offsets.data();
+    d.flops = to_c(handle.flops);
+    d.compression = to_c(handle.compression);
+    d.max_row_size = handle.max_row_size;
+    d.avg_row_size = handle.avg_row_size;
+    d.avg_row_size_estimate = handle.avg_row_size_estimate;
+    d.symbolic_choice = to_c(handle.symbolic_choice);
+    d.numeric_choice = to_c(handle.numeric_choice);
+    d.config = to_c(handle.config);
+    d.symbolic_stats = spg_phase_stats{handle.symbolic_stats.ms, handle.symbolic_stats.pool_allocations,
+                                       handle.symbolic_stats.l2_inserts};
+    d.compress_ms = handle.compress_ms;
+    d.per_row_flops = handle.flops.per_row_flops.size() == static_cast<size_t>(handle.m)
+        ? handle.flops.per_row_flops.data()
+        : nullptr;
+    auto e = std::make_unique<Entry>();
+    check(spg_handle_import(&d, &e->h, nullptr));
+    return e;
+}
+
 } // namespace
 
 std::pair<index_t, flops_t> flat_position(std::span<const flops_t> prefix, flops_t t)
@@ -158,12 +407,15 @@ SpgemmHandle symbolic(const CsrMatrix& a, const CsrMatrix& b, const SpgemmConfig
 {
     if (a.num_cols != b.num_rows)
         throw ContractError("symbolic: inner dimensions do not match");
-    DevCsr da(a), db(b);
+    Cache& cache = Cache::get();
+    std::lock_guard<std::mutex> lk(cache.mu);
+    auto e = std::make_unique<Entry>();
+    e->stg = &cache.staging();
+    e->upload(a, b);
     const spg_config c = to_c(cfg);
-    HandleGuard g;
-    check(spg_symbolic(&da.view, &db.view, &c, &g.h, nullptr));
+    check(spg_symbolic(&e->a.view, e->bview(), &c, &e->h, nullptr));
     spg_handle_info info{};
-    check(spg_handle_info_get(g.h, &info));
+    check(spg_handle_info_get(e->h, &info));
 
     SpgemmHandle h;
     h.config = cfg;
@@ -173,10 +425,10 @@ SpgemmHandle symbolic(const CsrMatrix& a, const CsrMatrix& b, const SpgemmConfig
     h.nnz_a = info.nnz_a;
     h.nnz_b = info.nnz_b;
     h.c_row_offsets.resize(static_cast<size_t>(info.m) + 1);
-    check(spg_handle_copy_row_offsets(g.h, h.c_row_offsets.data()));
+    check(spg_handle_copy_row_offsets(e->h, h.c_row_offsets.data()));
     h.flops.per_row_flops.resize(static_cast<size_t>(info.m));
     if (info.m > 0)
-        check(spg_handle_copy_per_row_flops(g.h, h.flops.per_row_flops.data()));
+        check(spg_handle_copy_per_row_flops(e->h, h.flops.per_row_flops.data()));
     h.flops.total_flops = info.flops.total_flops;
     h.flops.max_row_flops = info.flops.max_row_flops;
     h.flops.avg_degree_a = info.flops.avg_degree_a;
@@ -195,61 +447,68 @@ SpgemmHandle symbolic(const CsrMatrix& a, const CsrMatrix& b, const SpgemmConfig
     h.symbolic_stats.pool_allocations = info.symbolic_stats.pool_allocations;
     h.symbolic_stats.l2_inserts = info.symbolic_stats.l2_inserts;
     h.compress_ms = info.compress_ms;
+    // keep the device handle and the uploaded operands for numeric() on this
+    // handle (the vector's buffer moves with the returned handle)
+    e->key = h.c_row_offsets.data();
+    e->digest = handle_digest(h);
+    e->fresh_a = &a;
+    e->fresh_b = &b;
+    cache.insert(std::move(e));
     return h;
 }
 
-CsrMatrix numeric(const CsrMatrix& a, const CsrMatrix& b, const SpgemmHandle& handle, PhaseStats* stats)
+namespace {
+
+// same_call: a multiply() running numeric right after its own symbolic, so the
+// operands symbolic() uploaded are still the caller's (numeric() alone always
+// uploads: the caller may have changed values or structure since)
+CsrMatrix numeric_impl(const CsrMatrix& a, const CsrMatrix& b, const SpgemmHandle& handle, PhaseStats* stats,
+                       bool same_call)
 {
     // engine.cpp:451-453, checked before any device work
     if (a.num_rows != handle.m || a.num_cols != handle.n || b.num_rows != handle.n || b.num_cols != handle.k
         || a.nnz() != handle.nnz_a || b.nnz() != handle.nnz_b)
         throw ReuseError("numeric: operands do not match the symbolic handle");
 
-    spg_handle_desc d{};
-    d.m = handle.m;
-    d.n = handle.n;
-    d.k = handle.k;
-    d.nnz_a = handle.nnz_a;
-    d.nnz_b = handle.nnz_b;
-    d.c_row_offsets = handle.c_row_offsets.data();
-    d.flops = to_c(handle.flops);
-    d.compression = to_c(handle.compression);
-    d.max_row_size = handle.max_row_size;
-    d.avg_row_size = handle.avg_row_size;
-    d.avg_row_size_estimate = handle.avg_row_size_estimate;
-    d.symbolic_choice = to_c(handle.symbolic_choice);
-    d.numeric_choice = to_c(handle.numeric_choice);
-    d.config = to_c(handle.config);
-    d.symbolic_stats = spg_phase_stats{handle.symbolic_stats.ms, handle.symbolic_stats.pool_allocations,
-                                       handle.symbolic_stats.l2_inserts};
-    d.compress_ms = handle.compress_ms;
-    HandleGuard g;
-    check(spg_handle_import(&d, &g.h, nullptr));
-
-    DevCsr da(a), db(b);
-    const int64_t nnz = handle.nnz_c();
-    int32_t* dc = nullptr;
-    double* dv = nullptr;
-    cuda(cudaMalloc(&dc, sizeof(int32_t) * static_cast<size_t>(nnz > 0 ? nnz : 1)));
-    cuda(cudaMalloc(&dv, sizeof(double) * static_cast<size_t>(nnz > 0 ? nnz : 1)));
-    spg_phase_stats st{};
-    const int rc = spg_numeric(g.h, &da.view, &db.view, dc, dv, &st, nullptr);
-    CsrMatrix c;
-    if (rc == SPG_OK) {
-        c.num_rows = handle.m;
-        c.num_cols = handle.k;
-        c.row_offsets = handle.c_row_offsets;
-        c.col_indices.resize(static_cast<size_t>(nnz));
-        c.values.resize(static_cast<size_t>(nnz));
-        if (nnz > 0) {
-            cudaMemcpy(c.col_indices.data(), dc, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost);
-            cudaMemcpy(c.values.data(), dv, sizeof(double) * nnz, cudaMemcpyDeviceToHost);
-        }
-        c.sorted_rows = handle.config.sort_output;
+    Cache& cache = Cache::get();
+    std::lock_guard<std::mutex> lk(cache.mu);
+    const uint64_t dig = handle_digest(handle);
+    Entry* e = cache.find(handle.c_row_offsets.data(), dig);
+    if (!e) {
+        auto ne = import_entry(handle);
+        ne->stg = &cache.staging();
+        ne->key = handle.c_row_offsets.data();
+        ne->digest = dig;
+        e = cache.insert(std::move(ne));
     }
-    cudaFree(dc);
-    cudaFree(dv);
-    check(rc);
+    if (!(same_call && e->fresh_a == &a && e->fresh_b == &b))
+        e->upload(a, b);
+    e->fresh_a = e->fresh_b = nullptr;
+    const int64_t nnz = handle.nnz_c();
+    const size_t need = static_cast<size_t>(nnz > 0 ? nnz : 1);
+    if (need > e->cap_c) {
+        cudaFree(e->dc);
+        cudaFree(e->dv);
+        e->dc = nullptr;
+        e->dv = nullptr;
+        cuda(cudaMalloc(&e->dc, sizeof(int32_t) * need));
+        cuda(cudaMalloc(&e->dv, sizeof(double) * need));
+        e->cap_c = need;
+    }
+    spg_phase_stats st{};
+    check(spg_numeric(e->h, &e->a.view, e->bview(), e->dc, e->dv, stats ? &st : nullptr, nullptr));
+    CsrMatrix c;
+    c.num_rows = handle.m;
+    c.num_cols = handle.k;
+    c.row_offsets = handle.c_row_offsets;
+    c.col_indices.resize(static_cast<size_t>(nnz));
+    c.values.resize(static_cast<size_t>(nnz));
+    if (nnz > 0) {
+        e->stg->down(c.col_indices.data(), e->dc, sizeof(int32_t) * nnz, nullptr);
+        e->stg->down(c.values.data(), e->dv, sizeof(double) * nnz, nullptr);
+    }
+    check(spg_handle_check(e->h)); // errors of an asynchronous pass (the reference's logic_error)
+    c.sorted_rows = handle.config.sort_output;
     if (stats) {
         stats->ms = st.ms;
         stats->pool_allocations = st.pool_allocations;
@@ -258,11 +517,18 @@ CsrMatrix numeric(const CsrMatrix& a, const CsrMatrix& b, const SpgemmHandle& ha
     return c;
 }
 
+} // namespace
+
+CsrMatrix numeric(const CsrMatrix& a, const CsrMatrix& b, const SpgemmHandle& handle, PhaseStats* stats)
+{
+    return numeric_impl(a, b, handle, stats, false);
+}
+
 MultiplyResult multiply(const CsrMatrix& a, const CsrMatrix& b, const SpgemmConfig& cfg)
 {
     MultiplyResult r;
     r.handle = symbolic(a, b, cfg);
-    r.c = numeric(a, b, r.handle, &r.numeric_stats);
+    r.c = numeric_impl(a, b, r.handle, &r.numeric_stats, true);
     return r;
 }
 

@@ -466,15 +466,6 @@ void ensure_pool(DevPool& pool, const L2Spec& P, cudaStream_t st)
     cuda_check(cudaMemsetAsync(pool.states, 0, sizeof(int) * P.num_chunks, st), "pool states");
 }
 
-void free_pool(DevPool& pool)
-{
-    if (pool.base)
-        cudaFree(pool.base);
-    if (pool.states)
-        cudaFree(pool.states);
-    pool = DevPool{};
-}
-
 // Per-thread pinned scratch for the symbolic phase's small host reads.
 // Pinned allocation and release synchronise the whole device (they would wait
 // for unrelated copies on other streams, e.g. an overlapped upload), so the
@@ -571,8 +562,7 @@ struct spg_handle {
     bool num_slab = false;      // heavy rows by column slabs (kk_slab.cu) instead of buckets
     bool b_sorted = false;      // symbolic saw every referenced B row column-sorted
     int64_t max_a_row = 0;      // longest A row (slab cursors)
-    int32_t* slab_scratch = nullptr;
-    int slab_grid = 0;
+    SlabPlan slab;              // work items and per-warp cursor scratch
     int heavy_nb = 0;
     int64_t heavy_stage = 0; // staging products
     int64_t heavy_cap = 0;
@@ -590,14 +580,27 @@ struct spg_handle {
     unsigned long long* d_fp = nullptr; // [4]: A, B of the current pass; A, B recorded
     unsigned long long* h_fp = nullptr; // pinned [2 + DevCounters]
 
+    void free_slab()
+    {
+        for (void* p : {static_cast<void*>(slab.items), slab.scratch, static_cast<void*>(slab.split_out),
+                        static_cast<void*>(slab.split_done)})
+            if (p)
+                cudaFreeAsync(p, stream);
+        slab = SlabPlan{};
+    }
+
     void free_replay()
     {
+        // device buffers are stream-ordered (cudaMallocAsync); the pinned
+        // readback needs the stream drained first
         for (void* p : {d_map, static_cast<void*>(d_prod_off), static_cast<void*>(d_ccache),
                         static_cast<void*>(d_rctr), static_cast<void*>(d_fp)})
             if (p)
-                cudaFree(p);
-        if (h_fp)
+                cudaFreeAsync(p, stream);
+        if (h_fp) {
+            cudaStreamSynchronize(stream);
             cudaFreeHost(h_fp);
+        }
         d_map = nullptr;
         d_prod_off = nullptr;
         d_ccache = nullptr;
@@ -607,30 +610,32 @@ struct spg_handle {
         replay_ready = false;
     }
 
+    // Every device buffer comes from the stream-ordered allocator and is
+    // released on the handle's stream: destroying a handle neither waits for
+    // the device nor synchronises it (cudaFree would), so a NoReuse multiply
+    // loop keeps the GPU busy across handles.
     ~spg_handle()
     {
         free_replay();
-        if (heavy_stage_buf)
-            cudaFree(heavy_stage_buf);
-        if (slab_scratch)
-            cudaFree(slab_scratch);
-        if (d_rowptr)
-            cudaFree(d_rowptr);
-        if (d_prf)
-            cudaFree(d_prf);
-        if (d_ctr)
-            cudaFree(d_ctr);
-        if (d_num_list)
-            cudaFree(d_num_list);
-        if (d_empty_list)
-            cudaFree(d_empty_list);
-        free_pool(num_pool);
+        free_slab();
+        for (void* p : {heavy_stage_buf, static_cast<void*>(d_rowptr), static_cast<void*>(d_prf),
+                        static_cast<void*>(d_ctr), static_cast<void*>(d_num_list),
+                        static_cast<void*>(d_empty_list), static_cast<void*>(num_pool.base),
+                        static_cast<void*>(num_pool.states)})
+            if (p)
+                cudaFreeAsync(p, stream);
     }
 };
 
 namespace {
 
-void build_numeric_plan(spg_handle* h, cudaStream_t st)
+// Work items of the column-slab kernel (one per heavy row, long rows cut into
+// column parts) and the per-warp cursor scratch.  Needs the handle's A row
+// offsets only through max_a_row and the items' part counts, which are a
+// performance choice: any A of the handle's shape runs correctly.
+void build_slab_plan(spg_handle* h, const int64_t* a_rowptr, cudaStream_t st);
+
+void build_numeric_plan(spg_handle* h, cudaStream_t st, const int64_t* a_rowptr = nullptr)
 {
     const spg_config& cfg = h->info.config;
     int acc;
@@ -658,14 +663,12 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
     // fit 32-bit staging offsets
     h->num_heavy = false;
     h->num_slab = false;
+    h->free_slab();
     if (fast && !forced && h->num.l2_class >= 0 && h->b_sorted && h->max_a_row > 0) {
-        // column slabs: no row-size limit, products read once
+        // column slabs: no row-size limit, products read once (work items are
+        // built below, once the heavy rows are listed largest first)
         h->num_heavy = true;
         h->num_slab = true;
-        h->slab_grid = numeric_slab_blocks_per_sm() * sm_count();
-        if (h->slab_scratch)
-            cudaFreeAsync(h->slab_scratch, st);
-        h->slab_scratch = dalloc<int32_t>(static_cast<size_t>(h->slab_grid) * 2 * h->max_a_row, st, "slab cursors");
     } else if (fast && !forced && h->num.l2_class >= 0) {
         const int64_t cap = std::max<int64_t>(h->info.flops.max_row_flops, 1);
         if (h->info.max_row_size <= kHeavyMaxRow && cap < (int64_t{1} << 31)) {
@@ -677,7 +680,6 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
     }
     // slot replay (kk_replay.cu) for the Auto Thread-Sequential plan when all
     // rows run in warp tables and slots fit two bytes
-    cudaStreamSynchronize(st);
     h->free_replay();
     h->numeric_calls = 0;
     h->replay_eligible = fast && !forced && !flat && h->num.l2_class < 0 && !h->num_heavy && h->d_prf
@@ -715,6 +717,50 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st)
             cuda_check(sort_rows_by_flops_desc(h->d_num_list + hc.off, hc.count, h->d_prf, st), "heavy row order");
         }
     }
+    if (h->num_slab && a_rowptr)
+        build_slab_plan(h, a_rowptr, st); // else at the first numeric call (its A)
+}
+
+void build_slab_plan(spg_handle* h, const int64_t* a_rowptr, cudaStream_t st)
+{
+    const PhaseClass& hc = h->num.classes[h->num.l2_class];
+    SlabPlan& P = h->slab;
+    P.max_a_row = (h->max_a_row + 3) / 4 * 4; // keeps every warp's int64 cursor arrays 8-byte aligned
+    int64_t* off = dalloc<int64_t>(hc.count + 1, st, "slab item offsets");
+    cuda_check(build_slab_items(h->d_num_list + hc.off, hc.count, a_rowptr, h->d_rowptr, h->info.k, off, nullptr,
+                                nullptr, st),
+               "slab parts");
+    int64_t n_items = 0;
+    cuda_check(cudaMemcpyAsync(&n_items, off + hc.count, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "items");
+    cuda_check(cudaStreamSynchronize(st), "slab plan sync");
+    P.n_items = n_items;
+    P.items = dalloc<int4>(std::max<int64_t>(n_items, 1), st, "slab items");
+    auto* nsplit = dalloc<unsigned long long>(1, st, "split count");
+    cuda_check(cudaMemsetAsync(nsplit, 0, sizeof(unsigned long long), st), "memset");
+    cuda_check(build_slab_items(h->d_num_list + hc.off, hc.count, a_rowptr, h->d_rowptr, h->info.k, off, P.items,
+                                nsplit, st),
+               "slab items");
+    unsigned long long n_split = 0;
+    cuda_check(cudaMemcpyAsync(&n_split, nsplit, sizeof(n_split), cudaMemcpyDeviceToHost, st), "split count");
+    cuda_check(cudaStreamSynchronize(st), "slab plan sync");
+    cudaFreeAsync(off, st);
+    cudaFreeAsync(nsplit, st);
+    P.n_split = static_cast<int64_t>(n_split);
+    if (P.n_split > 0) {
+        P.split_out = dalloc<unsigned long long>(P.n_split, st, "split rows");
+        P.split_done = dalloc<unsigned int>(P.n_split, st, "split rows");
+    }
+    // resident warps, bounded so the cursor scratch takes at most a quarter of
+    // the free memory
+    const int per_cta = slab_warps_per_cta();
+    int64_t warps = numeric_slab_warps();
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t per_warp = static_cast<size_t>(std::max<int64_t>(P.max_a_row, 1)) * slab_scratch_per_entry();
+    const int64_t by_mem = static_cast<int64_t>(free_b / 4 / per_warp) / per_cta * per_cta;
+    warps = std::max<int64_t>(per_cta, std::min(warps, by_mem));
+    P.warps = warps;
+    P.scratch = dalloc<unsigned char>(static_cast<size_t>(warps) * per_warp, st, "slab cursors");
 }
 
 ReplayLaunch replay_launch(spg_handle* h, const spg_csr* a, const spg_csr* b, int32_t* c_cols, double* c_vals)
@@ -769,7 +815,7 @@ void record_replay(spg_handle* h, const spg_csr* a, const spg_csr* b, int32_t* c
         return;
     }
     void* p = nullptr;
-    if (cudaMalloc(&p, map_bytes) != cudaSuccess) {
+    if (cudaMallocAsync(&p, map_bytes, st) != cudaSuccess) {
         cudaGetLastError();
         h->replay_eligible = false;
         return;
@@ -1174,7 +1220,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         I.symbolic_stats.pool_allocations = static_cast<int64_t>(hctr->pool_allocations);
         I.symbolic_stats.l2_inserts = static_cast<int64_t>(hctr->l2_inserts);
         spg_resolve_config(SPG_PHASE_NUMERIC, k, &I.flops, &R, &cfg, I.max_row_size, &I.numeric_choice);
-        build_numeric_plan(h, st);
+        build_numeric_plan(h, st, a->row_offsets);
         *out = h;
     });
     if (rc != SPG_OK) {
@@ -1245,6 +1291,8 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
                        "replay numeric");
             replayed = true;
         }
+        if (h->num_slab && !h->slab.items)
+            build_slab_plan(h, a->row_offsets, st); // handle re-planned without A (set_numeric)
         if (h->n_empty > 0 && row_hi > row_lo)
             cuda_check(launch_check_empty_rows(h->d_empty_list, h->n_empty, a->row_offsets, a->col_indices,
                                                b->row_offsets, full ? 0 : row_lo, full ? 0 : row_hi, h->d_ctr, st),
@@ -1276,9 +1324,7 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
             L.grid = pc.grid;
             L.l2 = pc.l2;
             if (pc.l2 && h->num_slab) {
-                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(h->slab_grid, pc.count)));
-                cuda_check(launch_numeric_slab(L, h->slab_scratch, h->max_a_row, I.k, h->d_prf, grid, st),
-                           "numeric slab kernel");
+                cuda_check(launch_numeric_slab(L, h->slab, I.k, h->d_prf, st), "numeric slab kernel");
             } else if (pc.l2 && h->num_heavy) {
                 const int64_t resident = int64_t{numeric_heavy_blocks_per_sm(h->heavy_nb)} * sm_count();
                 const int64_t want = std::max<int64_t>(1, std::min<int64_t>(resident, pc.count));
@@ -1449,6 +1495,12 @@ int spg_handle_import(const spg_handle_desc* d, spg_handle_t* out, void* stream)
         h->d_ctr = dalloc<DevCounters>(1, st, "counters");
         I.d_c_row_offsets = h->d_rowptr;
         I.d_per_row_flops = nullptr;
+        if (d->per_row_flops && d->m > 0) {
+            h->d_prf = dalloc<int64_t>(d->m, st, "per-row flops");
+            cuda_check(cudaMemcpyAsync(h->d_prf, d->per_row_flops, sizeof(int64_t) * d->m, cudaMemcpyHostToDevice, st),
+                       "upload per-row flops");
+            I.d_per_row_flops = h->d_prf;
+        }
         cuda_check(cudaMemcpyAsync(h->d_rowptr, d->c_row_offsets, sizeof(int64_t) * (int64_t{d->m} + 1),
                                    cudaMemcpyHostToDevice, st),
                    "upload row offsets");
@@ -1459,8 +1511,14 @@ int spg_handle_import(const spg_handle_desc* d, spg_handle_t* out, void* stream)
         cuda_check(cudaStreamSynchronize(st), "import sync");
         cudaFreeAsync(d_stot, st);
         I.max_row_size = std::max<int64_t>(I.max_row_size, static_cast<int64_t>(h->size_hist.max_size));
-        // the reference's numeric takes its choice from the handle as is
-        h->numeric_forced = true;
+        // the reference's numeric takes its choice from the handle as is: an
+        // Auto handle whose choice is the resolved one keeps the GPU plan, an
+        // edited choice (acceptance_main.cpp:417-425) runs as forced
+        spg_resolved auto_choice{};
+        spg_resolve_config(SPG_PHASE_NUMERIC, I.k, &I.flops, &I.compression, &I.config, I.max_row_size,
+                           &auto_choice);
+        h->numeric_forced = !(I.config.accumulator == SPG_ACC_AUTO &&
+                              std::memcmp(&auto_choice, &I.numeric_choice, sizeof(spg_resolved)) == 0);
         build_numeric_plan(h, st);
         *out = h;
     });
@@ -1494,10 +1552,7 @@ int spg_handle_replay_state(spg_handle_t h)
 
 void spg_handle_destroy(spg_handle_t h)
 {
-    if (h) {
-        cudaStreamSynchronize(h->stream);
-        delete h;
-    }
+    delete h; // stream-ordered release (see ~spg_handle)
 }
 
 int spg_row_flops(const spg_csr* a, const spg_csr* b, int64_t* d_out, void* stream)
@@ -1536,6 +1591,19 @@ int spg_transpose(const spg_csr* a, int64_t* d_t_row_offsets, int32_t* d_t_cols,
         cuda_check(launch_transpose_fill(a->num_rows, a->num_cols, a->row_offsets, a->col_indices, a->values,
                                          d_t_row_offsets, d_t_cols, d_t_vals, static_cast<int64_t>(hs.max_size), st),
                    "transpose fill");
+    });
+}
+
+int spg_row_digests(int32_t m, const int64_t* d_row_offsets, const int32_t* d_cols, const double* d_vals,
+                    uint64_t* d_out, void* stream)
+{
+    return guarded([&] {
+        if (m < 0 || (m > 0 && (!d_row_offsets || !d_out)))
+            fail(SPG_ERR_CONTRACT, "row_digests: bad argument");
+        require_device();
+        cuda_check(launch_row_digests(m, d_row_offsets, d_cols, d_vals, reinterpret_cast<unsigned long long*>(d_out),
+                                      static_cast<cudaStream_t>(stream)),
+                   "row digests");
     });
 }
 

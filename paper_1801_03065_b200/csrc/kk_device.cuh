@@ -56,6 +56,39 @@ __device__ __forceinline__ void raise_error(DevCounters* c, int code)
     atomicCAS(&c->error, 0, code);
 }
 
+// ---- cache policy for the numeric kernels ------------------------------------
+// B rows are re-read by every A row that references them (27 times on a 3D
+// stencil) within a short window of rows, while C (6 GB on config 2) is
+// written once: B's loads carry an L2 evict_last hint and C's stores are
+// streaming (evict-first), so the C stream does not push B's working band out
+// of L2.  -DKK_NO_CACHE_HINTS builds the plain variant (A/B measurements).
+#ifndef KK_NO_CACHE_HINTS
+__device__ __forceinline__ uint64_t l2_keep_policy()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int32_t ldg_keep(const int32_t* ptr, uint64_t pol)
+{
+    int32_t v;
+    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ldg_keep(const double* ptr, uint64_t pol)
+{
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+    return v;
+}
+template <class T> __device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
+#else
+__device__ __forceinline__ uint64_t l2_keep_policy() { return 0; }
+__device__ __forceinline__ int32_t ldg_keep(const int32_t* ptr, uint64_t) { return __ldg(ptr); }
+__device__ __forceinline__ double ldg_keep(const double* ptr, uint64_t) { return __ldg(ptr); }
+template <class T> __device__ __forceinline__ void st_stream(T* p, T v) { *p = v; }
+#endif
+
 // Multiplicative (Fibonacci) hash.  The reference hashes with key & mask
 // (accumulators.hpp:92,197), which degenerates on stencils (10-27 probes per
 // insert); the accumulated sets and values do not depend on it.

@@ -134,6 +134,7 @@ template <bool kCas>
 __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    const uint64_t pol = l2_keep_policy(); // B stays in L2 while C streams out
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     unsigned char* region = smem + (size_t)wib * L.lay.bytes;
@@ -190,8 +191,8 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
                         int32_t key = 0;
                         double v = 0.0;
                         if (valid) {
-                            key = __ldg(L.b_cols + rq.x + t0 + lane);
-                            v = __dmul_rn(a, __ldg(L.b_vals + rq.x + t0 + lane));
+                            key = ldg_keep(L.b_cols + rq.x + t0 + lane, pol);
+                            v = __dmul_rn(a, ldg_keep(L.b_vals + rq.x + t0 + lane, pol));
                         }
                         num_step<kCas>(valid, key, v, keys, vals, slot_of, tmask, shift, cap, cnt);
                     }
@@ -209,12 +210,12 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
                 len0 = static_cast<int32_t>(r0.y);
                 len1 = static_cast<int32_t>(r1.y);
                 if (lane < len0) {
-                    k0 = __ldg(L.b_cols + r0.x + lane);
-                    v0 = __ldg(L.b_vals + r0.x + lane);
+                    k0 = ldg_keep(L.b_cols + r0.x + lane, pol);
+                    v0 = ldg_keep(L.b_vals + r0.x + lane, pol);
                 }
                 if (lane < len1) {
-                    k1 = __ldg(L.b_cols + r1.x + lane);
-                    v1 = __ldg(L.b_vals + r1.x + lane);
+                    k1 = ldg_keep(L.b_cols + r1.x + lane, pol);
+                    v1 = ldg_keep(L.b_vals + r1.x + lane, pol);
                 }
             }
             for (int q = 0; q < na; ++q) {
@@ -224,8 +225,8 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
                     const longlong2 r2 = stage->row[q + 2];
                     len2 = static_cast<int32_t>(r2.y);
                     if (lane < len2) {
-                        k2 = __ldg(L.b_cols + r2.x + lane);
-                        v2 = __ldg(L.b_vals + r2.x + lane);
+                        k2 = ldg_keep(L.b_cols + r2.x + lane, pol);
+                        v2 = ldg_keep(L.b_vals + r2.x + lane, pol);
                     }
                 }
                 num_step<kCas>(lane < len0, k0, __dmul_rn(stage->a[q], v0), keys, vals, slot_of, tmask, shift,
@@ -245,8 +246,8 @@ __global__ void __launch_bounds__(256) numeric_lp_seq_kernel(const RowLaunch L)
         const int32_t used = cnt < cap ? cnt : cap;
         for (int32_t q = lane; q < used; q += 32) {
             const int32_t s = slot_of[q];
-            L.c_cols[cbase + q] = keys[s];
-            L.c_vals[cbase + q] = vals[s];
+            st_stream(L.c_cols + cbase + q, keys[s]);
+            st_stream(L.c_vals + cbase + q, vals[s]);
             keys[s] = kEmpty;
         }
         __syncwarp();
@@ -390,6 +391,7 @@ __device__ __forceinline__ void num_window(bool valid, int32_t key, double v, in
 __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    const uint64_t pol = l2_keep_policy(); // B stays in L2 while C streams out
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     unsigned char* region = smem + (size_t)wib * L.lay.bytes;
@@ -425,8 +427,8 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
             double v = 0.0;
             if (valid) {
                 const int64_t q = base + (t - e);
-                key = __ldg(L.b_cols + q);
-                v = __dmul_rn(a, __ldg(L.b_vals + q));
+                key = ldg_keep(L.b_cols + q, pol);
+                v = __dmul_rn(a, ldg_keep(L.b_vals + q, pol));
             }
             num_window(valid, key, v, keys, vals, slot_of, tmask, shift, cap, cnt, lane);
         }
@@ -437,8 +439,8 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
         const int32_t used = cnt < cap ? cnt : cap;
         for (int32_t q = lane; q < used; q += 32) {
             const int32_t s = slot_of[q];
-            L.c_cols[cbase + q] = keys[s];
-            L.c_vals[cbase + q] = vals[s];
+            st_stream(L.c_cols + cbase + q, keys[s]);
+            st_stream(L.c_vals + cbase + q, vals[s]);
             keys[s] = kEmpty;
         }
         __syncwarp();

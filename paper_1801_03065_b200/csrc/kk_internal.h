@@ -111,6 +111,8 @@ cudaError_t launch_transpose_fill(int32_t m, int32_t n, const int64_t* rowptr, c
 cudaError_t launch_col_range(int32_t m, const int64_t* a_rowptr, const int32_t* a_cols, int* out2, cudaStream_t st);
 cudaError_t launch_row_bucket_hist(int32_t m, const int64_t* rowptr, ScanTotals* tot,
                                    cudaStream_t st);
+cudaError_t launch_row_digests(int32_t m, const int64_t* rowptr, const int32_t* cols, const double* vals,
+                               unsigned long long* out, cudaStream_t st);
 cudaError_t launch_collect_empty_rows(int32_t m, const int64_t* c_rowptr, int32_t* list, unsigned long long* count,
                                       cudaStream_t st);
 cudaError_t launch_check_empty_rows(const int32_t* list, int64_t n, const int64_t* a_rowptr, const int32_t* a_cols,
@@ -135,9 +137,24 @@ cudaError_t sort_rows_by_flops_desc(int32_t* list, int64_t n, const int64_t* prf
 int numeric_heavy_blocks_per_sm(int32_t nb);
 
 // heavy rows by column slabs (kk_slab.cu); needs column-sorted B rows
-cudaError_t launch_numeric_slab(const RowLaunch& L, int32_t* scratch, int64_t max_a_row, int64_t k,
-                                const int64_t* prf, int grid, cudaStream_t st);
-int numeric_slab_blocks_per_sm();
+struct SlabPlan {
+    int4* items = nullptr;          // {row, part, parts, split slot}
+    int64_t n_items = 0;
+    void* scratch = nullptr;        // per warp cursor state
+    int64_t max_a_row = 0;
+    int64_t warps = 0;              // resident warps (multiple of the CTA's)
+    unsigned long long* split_out = nullptr;
+    unsigned int* split_done = nullptr;
+    int64_t n_split = 0;
+};
+cudaError_t build_slab_items(const int32_t* list, int64_t n, const int64_t* a_rowptr, const int64_t* c_rowptr,
+                             int64_t k, int64_t* item_off, int4* items, unsigned long long* split_count,
+                             cudaStream_t st);
+cudaError_t launch_numeric_slab(const RowLaunch& L, const SlabPlan& P, int64_t k, const int64_t* prf,
+                                cudaStream_t st);
+int numeric_slab_warps();
+int slab_warps_per_cta();
+size_t slab_scratch_per_entry();
 
 // structure-reuse replay (kk_replay.cu)
 struct ReplayLaunch {

@@ -1046,6 +1046,58 @@ cudaError_t launch_check_empty_rows(const int32_t* list, int64_t n, const int64_
 }
 
 // ---------------------------------------------------------------------------
+// Per-row canonical digests (the device side of oracle.cpp:105-159's
+// canonicalize + compare): an order-independent 64-bit hash of each row's
+// (column, value bits) set plus its length, so a row in any column order has
+// the digest of its sorted form.  The oracle computes the same function on the
+// CPU (oracle/spgemm_oracle.c orc_row_digests); equal digests mean equal
+// sorted columns and bitwise-equal values.  Warp per row, coalesced reads.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t dg_mix(uint64_t x)
+{
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+__global__ void __launch_bounds__(256) row_digest_kernel(int32_t m, const int64_t* __restrict__ rowptr,
+                                                         const int32_t* __restrict__ cols,
+                                                         const double* __restrict__ vals,
+                                                         unsigned long long* __restrict__ out)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
+        const int64_t lo = __ldg(rowptr + i), hi = __ldg(rowptr + i + 1);
+        uint64_t d = 0;
+        for (int64_t q = lo + lane; q < hi; q += 32) {
+            const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(__ldcs(vals + q)));
+            const uint32_t c = static_cast<uint32_t>(__ldcs(cols + q));
+            d += dg_mix((static_cast<uint64_t>(c) * 0x9E3779B97F4A7C15ull) ^ dg_mix(bits));
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1)
+            d += __shfl_xor_sync(kFull, d, off);
+        if (lane == 0)
+            out[i] = d + dg_mix(static_cast<uint64_t>(hi - lo) + 0x2545F4914F6CDD1Dull);
+    }
+}
+
+cudaError_t launch_row_digests(int32_t m, const int64_t* rowptr, const int32_t* cols, const double* vals,
+                               unsigned long long* out, cudaStream_t st)
+{
+    if (m <= 0)
+        return cudaSuccess;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((m + 7) / 8, (int64_t)sm_count() * 8));
+    row_digest_kernel<<<blocks, 256, 0, st>>>(m, rowptr, cols, vals, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // K7: per-row column sort (sort_output).  Warp per row; rows of up to
 // kSortSmem entries rank-sort in shared memory, longer rows rank-sort from a
 // global copy.

@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(256) replay_numeric_kernel(const ReplayLaunch 
         return; // structure changed since the map was recorded: the hashing kernels run
     const PosT* __restrict__ map = static_cast<const PosT*>(R.map);
     const double* __restrict__ b_vals = R.b_vals;
+    const uint64_t pol = l2_keep_policy(); // B values stay in L2; the map and C stream
     const int64_t nwarps = (int64_t)gridDim.x * R.wpb;
     for (int64_t i = R.row_lo + (int64_t)blockIdx.x * R.wpb + wib; i < R.row_hi; i += nwarps) {
         const int64_t cbase = __ldg(R.c_rowptr + i);
@@ -223,8 +224,8 @@ __global__ void __launch_bounds__(256) replay_numeric_kernel(const ReplayLaunch 
                     const longlong2 rq = stage->row[q];
                     const double a = stage->a[q];
                     for (int64_t t = lane; t < rq.y; t += 32) {
-                        const int32_t s = static_cast<int32_t>(__ldg(map + poff + t));
-                        const double v = __dmul_rn(a, __ldg(b_vals + rq.x + t));
+                        const int32_t s = static_cast<int32_t>(__ldcs(map + poff + t));
+                        const double v = __dmul_rn(a, ldg_keep(b_vals + rq.x + t, pol));
                         if (s < cap)
                             acc[s] = __dadd_rn(acc[s], v);
                         else
@@ -247,12 +248,12 @@ __global__ void __launch_bounds__(256) replay_numeric_kernel(const ReplayLaunch 
                 o1 = poff + len0;
                 o2 = o1 + len1;
                 if (lane < len0) {
-                    s0 = __ldg(map + poff + lane);
-                    v0 = __ldg(b_vals + r0.x + lane);
+                    s0 = __ldcs(map + poff + lane);
+                    v0 = ldg_keep(b_vals + r0.x + lane, pol);
                 }
                 if (lane < len1) {
-                    s1 = __ldg(map + o1 + lane);
-                    v1 = __ldg(b_vals + r1.x + lane);
+                    s1 = __ldcs(map + o1 + lane);
+                    v1 = ldg_keep(b_vals + r1.x + lane, pol);
                 }
             }
             for (int q = 0; q < na; ++q) {
@@ -262,8 +263,8 @@ __global__ void __launch_bounds__(256) replay_numeric_kernel(const ReplayLaunch 
                     const longlong2 r2 = stage->row[q + 2];
                     len2 = static_cast<int32_t>(r2.y);
                     if (lane < len2) {
-                        s2 = __ldg(map + o2 + lane);
-                        v2 = __ldg(b_vals + r2.x + lane);
+                        s2 = __ldcs(map + o2 + lane);
+                        v2 = ldg_keep(b_vals + r2.x + lane, pol);
                     }
                 }
                 if (lane < len0) {
@@ -295,8 +296,8 @@ __global__ void __launch_bounds__(256) replay_numeric_kernel(const ReplayLaunch 
         if (__any_sync(kFull, bad) && lane == 0)
             raise_error(R.ctr, kDevReplay);
         for (int32_t q = lane; q < cap; q += 32) {
-            R.c_cols[cbase + q] = __ldg(R.ccache + cbase + q);
-            R.c_vals[cbase + q] = acc[q];
+            st_stream(R.c_cols + cbase + q, __ldcs(R.ccache + cbase + q));
+            st_stream(R.c_vals + cbase + q, acc[q]);
         }
         __syncwarp();
     }

@@ -1,36 +1,41 @@
-// Heavy numeric rows by column slabs (sm_100a).
+// Heavy numeric rows by column slabs, one warp per slab sequence (sm_100a).
 //
 // Rows of C beyond the warp tables (R-MAT squares: 10^3..5*10^5 outputs per
-// row, 10^4..10^7 products) run one CTA per row, rows taken largest first
-// from a device queue.  The row's column domain is walked in SLABS
-// [c_lo, c_hi) sized so that a slab's distinct columns fit the CTA's
-// shared-memory table (~4K keys).  B's rows are column-sorted, so the part of
-// B row j that falls in a slab is one contiguous RUN; per A entry a cursor
-// remembers where the next slab's run starts, so every product is read once
-// in total and the per-slab bookkeeping is one short run-end search per A
-// entry.
+// row, 10^4..10^7 products) are walked in column SLABS [c_lo, c_hi) sized so
+// that a slab's distinct columns fit one warp's shared-memory table (~600 of
+// 1024 slots).  B's rows are column-sorted, so the part of B row j inside a
+// slab is one contiguous RUN; per A entry the warp keeps a cursor (where the
+// next slab's run starts) and the column found there, so an A entry whose B
+// row has nothing in the slab costs one coalesced scratch read, and every
+// product is read exactly once.
 //
-// Left-to-right value order (bitwise the reference's sums): inside
-// a slab the products are visited in the reference's (A position, B position)
-// order.  A chunk of 512 products is staged, partitioned by a hash of the
-// column into 8 classes with a STABLE counting sort (per-warp match ranks +
-// a 64-entry scan), and warp c owns class c: it folds its products into its
-// private table partition in product order (duplicates inside a 32-product
-// window folded by the lowest lane, lane order = product order).  A key lives
-// in exactly one partition, so every key's products are summed in product
-// order, starting from the first product.
+// Left-to-right value order (bitwise the reference's sums): one
+// warp accumulates a slab, visiting its products in the reference's
+// (A position, B position) order — runs one after another when they are long
+// (lanes over a run's entries: distinct keys, no conflicts), or 32-product
+// windows across several short runs with duplicate keys folded by the lowest
+// lane in lane (= product) order.  Every key's products are therefore summed
+// in product order starting from the first product.
 //
-// Slab width is adaptive: the first guess assumes uniform column density
-// (cap/k), later slabs rescale by the density just seen, and a slab whose
-// partition exceeds its key budget is abandoned (tables cleared, cursors not
-// advanced) and retried at half the width.  Rows come out slab by slab in
-// increasing column ranges (a slab's columns in partition/slot order); the
-// contract compares sorted rows.  The row's entry count is checked against
-// the symbolic structure.
+// Slab width is adaptive: the first guess assumes uniform column density,
+// each slab's product count (known before any product is folded) corrects it
+// with the last slab's keys-per-product ratio, later slabs rescale by the
+// density just seen, and a slab whose table overflows anyway is abandoned
+// (table cleared, cursors not advanced) and retried at half the width.
 //
-// A staged column below c_lo means a B row is not column-sorted (the run
-// ended early): the kernel raises kDevUnsorted — the host plans this kernel
-// only when the symbolic pass saw every referenced B row sorted.
+// Rows whose slab walk would be long for one warp (A-row length x row size
+// above kSplitWork) are cut into equal column PARTS walked by different warps
+// (cursors start at the part's first column, found by binary search).  A
+// part reserves its output block in the row when each slab completes, so the
+// columns of such a row come out grouped by slab in completion order; other
+// rows come out slab by slab in increasing column ranges.  The contract
+// compares sorted rows; the row's entry count is checked against the
+// symbolic structure.
+//
+// A B row that is not column-sorted makes a run end early and a later slab
+// meet a column below its lower bound: kDevUnsorted (the host plans this
+// kernel only when the symbolic pass saw every referenced B row sorted).
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 
@@ -41,94 +46,57 @@ namespace kk {
 
 namespace {
 
-constexpr int kSW = 8;                // warps per CTA = table partitions = key classes
-constexpr int kST = kSW * 32;         // threads
-constexpr int kTW = 1024;             // slots per partition
-constexpr int kTWMax = 768;           // keys per partition before the slab is abandoned
-constexpr int kXTarget = kSW * 480;   // target distinct keys per slab
-constexpr int kG = kST;               // A entries per group (one per thread in the run search)
-constexpr int kF = 2 * kST;           // products per staged chunk (two windows per warp)
+constexpr int kWarps = 8;           // independent warps per CTA
+constexpr int kTW = 1024;           // table slots per warp
+constexpr int kTWMax = 768;         // keys before a slab is abandoned
+constexpr int kX = 600;             // target distinct keys per slab
+constexpr double kSplitWork = 4e8;  // A-row length x row size per part
 
-struct __align__(16) SlabSmem {
-    int32_t keys[kSW][kTW];
-    double vals[kSW][kTW];
-    double sval[kF];
-    int32_t scol[kF];
-    int64_t qst[kG];      // first B position of each non-empty run of the group
-    double av[kG];        // A value of that run
-    int32_t roff[kG + 1]; // flat offset of each run inside the group (compacted, strictly increasing)
-    int32_t cnt[kSW][kSW]; // [staging warp][class] products of the chunk
-    long long wsum[kSW];
-    int32_t nkeys[kSW];
-    int64_t row;
-    int32_t ovf;
-};
+
 
 __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
-
-__device__ __forceinline__ int key_class(int32_t key)
-{
-    return static_cast<int>((static_cast<uint32_t>(key) * 0x9E3779B1u) >> 29);
-}
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ uint32_t key_slot(int32_t key)
 {
-    return (static_cast<uint32_t>(key) * 0x85EBCA6Bu) >> 22; // 10 bits, independent of the class
+    return (static_cast<uint32_t>(key) * 0x9E3779B1u) >> 22; // 10 bits
 }
 
-// block-wide exclusive scan of one int64 per thread; *total = the sum
-__device__ __forceinline__ long long block_scan(long long v, long long* wsum, long long* total)
-{
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    long long incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o)
-            incl += y;
-    }
-    if (lane == 31)
-        wsum[warp] = incl;
-    __syncthreads();
-    long long pre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kSW; ++w) {
-        const long long x = wsum[w];
-        pre += w < warp ? x : 0;
-        tot += x;
-    }
-    *total = tot;
-    __syncthreads();
-    return pre + incl - v;
-}
-
-// First q in [s, be) with cols[q] >= c_hi, for a column-sorted row (an
-// unsorted row is caught at staging).  Runs are mostly short: eight
-// independent loads first, then a galloping search.
-__device__ __forceinline__ int64_t run_end(const int32_t* __restrict__ cols, int64_t s, int64_t be, int64_t c_hi)
+// First q in [s, be) with cols[q] >= c, for a column-sorted row; *at = cols[q]
+// (INT_MAX when q == be).  Runs are mostly short: eight independent loads
+// first, then a galloping search.
+__device__ __forceinline__ int64_t run_end(const int32_t* __restrict__ cols, int64_t s, int64_t be, int64_t c,
+                                           int32_t* at)
 {
     int64_t q = s;
     for (int round = 0; round < 2; ++round) {
         const int64_t n = be - q;
-        if (n <= 0)
+        if (n <= 0) {
+            *at = INT_MAX;
             return be;
-        int32_t c[8];
+        }
+        int32_t v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-            c[u] = u < n ? __ldg(cols + q + u) : INT_MAX;
+            v[u] = u < n ? __ldg(cols + q + u) : INT_MAX;
         int first = 8;
+        int32_t fv = INT_MAX;
 #pragma unroll
         for (int u = 7; u >= 0; --u)
-            if (c[u] >= c_hi)
+            if (v[u] >= c) {
                 first = u;
-        if (first < 8 || n <= 8)
-            return q + (first < n ? first : n);
+                fv = v[u];
+            }
+        if (first < 8) {
+            *at = fv;
+            return q + first;
+        }
         q += 8;
     }
-    // gallop: cols[q - 1] < c_hi
+    // gallop: cols[q - 1] < c
     int64_t step = 16, lo = q - 1, hi = be;
     while (q + step - 1 < be) {
-        if (__ldg(cols + q + step - 1) >= c_hi) {
+        if (__ldg(cols + q + step - 1) >= c) {
             hi = q + step - 1;
             break;
         }
@@ -136,108 +104,188 @@ __device__ __forceinline__ int64_t run_end(const int32_t* __restrict__ cols, int
         q += step;
         step <<= 1;
     }
-    // cols[lo] < c_hi, hi == be or cols[hi] >= c_hi
-    while (hi - lo > 1) {
+    while (hi - lo > 1) { // cols[lo] < c, hi == be or cols[hi] >= c
         const int64_t mid = lo + ((hi - lo) >> 1);
-        if (__ldg(cols + mid) >= c_hi)
+        if (__ldg(cols + mid) >= c)
             hi = mid;
         else
             lo = mid;
     }
+    *at = hi < be ? __ldg(cols + hi) : INT_MAX;
     return hi;
 }
 
-// run of flat position f inside a group: roff strictly increasing, roff[0] = 0,
-// roff[nr] = total.  `hint` (warp-uniform, monotone) is the run of an earlier
-// window start; fw = this window's start (<= every lane's f).
-__device__ __forceinline__ int find_run(const int32_t* roff, int nr, int& hint, int32_t fw, int32_t f, int lane)
+// lower_bound by plain binary search (cursor of a part that starts mid-row)
+__device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ cols, int64_t lo, int64_t hi, int64_t c)
 {
-    for (;;) {
-        const int idx = hint + 1 + lane;
-        const int32_t b = idx <= nr ? roff[idx] : INT_MAX;
-        const uint32_t M = __ballot_sync(kFull, b <= fw);
-        hint += __popc(M);
-        if (M != kFull)
-            break;
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if (__ldg(cols + mid) < c)
+            lo = mid + 1;
+        else
+            hi = mid;
     }
-    // roff[hint] <= fw < roff[hint + 1]; run starts inside the window (at most
-    // 31, runs are non-empty)
-    const int idx = hint + 1 + lane;
-    const int32_t b = idx <= nr ? roff[idx] : INT_MAX;
-    uint32_t M2 = __ballot_sync(kFull, b <= fw + 31);
-    int p = hint;
-    while (M2) {
-        const int j = __ffs(M2) - 1;
-        M2 &= M2 - 1;
-        if (__shfl_sync(kFull, b, j) <= f)
-            ++p;
-    }
-    return p;
+    return lo;
 }
 
 } // namespace
 
-// Optional phase profile (-DKK_SLAB_PROF): thread 0 of every CTA adds clock
+// Optional phase profile (-DKK_SLAB_PROF): lane 0 of every warp adds clock
 // deltas and event counts; read with spg_debug_slab_prof.
 #ifdef KK_SLAB_PROF
 __device__ unsigned long long g_slab_prof[16];
 #define PROF_DECL unsigned long long prof_t = clock64();
 #define PROF_MARK(idx)                                                                                   \
     do {                                                                                                 \
-        if (threadIdx.x == 0) {                                                                          \
+        if (lane == 0) {                                                                                 \
             const unsigned long long now = clock64();                                                    \
             atomicAdd(&g_slab_prof[idx], now - prof_t);                                                  \
             prof_t = now;                                                                                \
         }                                                                                                \
     } while (0)
-#define PROF_RESET                                                                                       \
-    do {                                                                                                 \
-        if (threadIdx.x == 0)                                                                            \
-            prof_t = clock64();                                                                          \
-    } while (0)
 #define PROF_COUNT(idx, n)                                                                               \
     do {                                                                                                 \
-        if (threadIdx.x == 0)                                                                            \
+        if (lane == 0)                                                                                   \
             atomicAdd(&g_slab_prof[idx], (unsigned long long)(n));                                       \
     } while (0)
 #else
 #define PROF_DECL
 #define PROF_MARK(idx)
-#define PROF_RESET
 #define PROF_COUNT(idx, n)
 #endif
 
 struct SlabArgs {
-    int32_t* scratch;   // per CTA: cursors [max_a_row] + run ends [max_a_row] (int32, relative to the B row)
-    int64_t max_a_row;  // longest A row among the planned rows
+    const int4* items;  // {row, part, parts, split slot}
+    int64_t n_items;
+    unsigned char* scratch; // per warp: cursor state of up to max_a_row A entries
+    int64_t max_a_row;
     int64_t k;          // column domain
-    const int64_t* prf; // per-row flops (distinct-key estimate of the first slab), may be null
+    const int64_t* prf; // per-row flops (first slab's keys-per-product ratio), may be null
+    unsigned long long* split_out;  // per split row: output entries reserved so far
+    unsigned int* split_done;       // per split row: parts finished
 };
 
-__global__ void __launch_bounds__(kST, 2) numeric_slab_kernel(const RowLaunch L, const SlabArgs S)
+// per-warp scratch: a cursor per A entry (one 16-byte load per lane) and the
+// run list of the slab being planned (non-empty runs in A order)
+struct __align__(16) Cursor {
+    int64_t pos; // next unconsumed B position
+    int32_t rem; // B entries left in the row from pos
+    int32_t nxt; // column at pos (INT_MAX when none)
+};
+
+struct WarpScratch {
+    Cursor* cur;
+    int64_t* rs;  // run start (B position)
+    double* ra;   // A value of the run
+    int32_t* rl;  // run length
+    int32_t* rp;  // A entry of the run
+    int32_t* rnx; // column after the run (the entry's next cursor column)
+};
+
+constexpr size_t kScratchPerEntry = 16 + 8 + 8 + 4 + 4 + 4; // 44 B; max_a_row is a multiple of 4
+
+__device__ __forceinline__ WarpScratch warp_scratch(unsigned char* base, int64_t n)
+{
+    WarpScratch w;
+    w.cur = reinterpret_cast<Cursor*>(base);
+    w.rs = reinterpret_cast<int64_t*>(w.cur + n);
+    w.ra = reinterpret_cast<double*>(w.rs + n);
+    w.rl = reinterpret_cast<int32_t*>(w.ra + n);
+    w.rp = w.rl + n;
+    w.rnx = w.rp + n;
+    return w;
+}
+
+// shared memory per warp: the table and the slots its keys occupy (for an
+// O(keys) emission)
+struct __align__(16) WarpSmem {
+    int32_t keys[kTW];
+    double vals[kTW];
+    uint16_t used[kTWMax + 32];
+};
+
+// Fold one 32-product window into the warp table.  kDistinct: the window's
+// keys are distinct (all from one run).  New keys get their slot recorded in
+// used[nk...]; nk advances.
+template <bool kDistinct>
+__device__ __forceinline__ void fold(bool valid, int32_t key, double v, WarpSmem& t, int& nk, int lane)
+{
+    uint32_t grp = 0;
+    bool leader = valid;
+    if constexpr (!kDistinct) {
+        grp = __match_any_sync(kFull, valid ? key : (-1 - lane));
+        leader = valid && (__ffs(grp) - 1) == lane;
+    }
+    uint32_t slot = 0;
+    bool is_new = false;
+    if (leader) {
+        slot = key_slot(key);
+        for (;;) {
+            const int32_t kx = t.keys[slot];
+            if (kx == key)
+                break;
+            if (kx == kEmpty) {
+                const int32_t old = atomicCAS(&t.keys[slot], kEmpty, key);
+                if (old == kEmpty) {
+                    is_new = true;
+                    break;
+                }
+                if (old == key)
+                    break;
+            }
+            slot = (slot + 1) & (kTW - 1);
+        }
+    }
+    double acc = v;
+    if (leader && !is_new)
+        acc = __dadd_rn(t.vals[slot], v);
+    if constexpr (!kDistinct) {
+        // the rest of the group in lane order: ((acc + v2) + v3) ...
+        uint32_t rest = leader ? (grp & (grp - 1)) : 0u;
+        const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(rest)));
+        for (int rr = 0; rr < rounds; ++rr) {
+            const int src = rest ? __ffs(rest) - 1 : lane;
+            const double xv = __shfl_sync(kFull, v, src);
+            if (rest) {
+                acc = __dadd_rn(acc, xv);
+                rest &= rest - 1;
+            }
+        }
+    }
+    if (leader)
+        t.vals[slot] = acc;
+    const uint32_t nm = __ballot_sync(kFull, is_new);
+    if (is_new) {
+        const int q = nk + __popc(nm & lanemask_lt());
+        if (q < kTWMax + 32)
+            t.used[q] = static_cast<uint16_t>(slot);
+    }
+    nk += __popc(nm);
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const RowLaunch L, const SlabArgs S)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SlabSmem& sm = *reinterpret_cast<SlabSmem*>(smem_raw);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int32_t* cur = S.scratch + (size_t)blockIdx.x * 2 * S.max_a_row;
-    int32_t* endr = cur + S.max_a_row;
-    int32_t* mykeys = sm.keys[warp];
-    double* myvals = sm.vals[warp];
-
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem& tab = reinterpret_cast<WarpSmem*>(smem_raw)[wib];
+    const int64_t gw = (int64_t)blockIdx.x * kWarps + wib;
+    const WarpScratch ws = warp_scratch(S.scratch + (size_t)gw * S.max_a_row * kScratchPerEntry, S.max_a_row);
+    const uint64_t pol = l2_keep_policy();
     for (int t = lane; t < kTW; t += 32)
-        mykeys[t] = kEmpty;
+        tab.keys[t] = kEmpty;
     __syncwarp();
     PROF_DECL
 
     for (;;) {
-        if (threadIdx.x == 0)
-            sm.row = static_cast<int64_t>(atomicAdd(&L.ctr->next_row[0], 1ull));
-        __syncthreads();
-        const int64_t r = sm.row;
-        __syncthreads();
-        if (r >= L.nrows)
+        unsigned long long itu = 0;
+        if (lane == 0)
+            itu = atomicAdd(&L.ctr->next_row[0], 1ull);
+        const int64_t it = static_cast<int64_t>(__shfl_sync(kFull, itu, 0));
+        if (it >= S.n_items)
             break;
-        const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
+        const int4 item = S.items[it];
+        const int32_t i = item.x, part = item.y, parts = item.z, slot = item.w;
         if (L.row_hi > 0 && (i < L.row_lo || i >= L.row_hi))
             continue; // outside the requested row range (spg_numeric_rows)
         const int64_t cbase = __ldg(L.c_rowptr + i);
@@ -245,293 +293,297 @@ __global__ void __launch_bounds__(kST, 2) numeric_slab_kernel(const RowLaunch L,
         const int64_t abeg = __ldg(L.a_rowptr + i), aend = __ldg(L.a_rowptr + i + 1);
         const int64_t d = aend - abeg;
         if (d > S.max_a_row) { // plan / operand mismatch: the cursors would not fit
-            if (threadIdx.x == 0)
+            if (lane == 0)
                 raise_error(L.ctr, kDevRowOverflow);
             continue;
         }
-        int64_t emitted = 0;
-        int64_t c_lo = 0;
-        // first slab: all columns when the row fits one table, else the
-        // uniform-density guess (then corrected from the slab's product count)
-        int64_t W = cap <= kXTarget ? S.k : imax64(32, S.k * kXTarget / imax64(cap, 1));
-        // distinct keys per product: the row's ratio first, then the last slab's
+        const int64_t C_lo = S.k * part / parts, C_hi = S.k * (part + 1) / parts;
+        // ---- cursors at the part's first column ----
+        for (int64_t p0 = 0; p0 < d; p0 += 32) {
+            const int64_t p = p0 + lane;
+            if (p < d) {
+                const int32_t j = __ldg(L.a_cols + abeg + p);
+                const int64_t bs = __ldg(L.b_rowptr + j), be = __ldg(L.b_rowptr + j + 1);
+                const int64_t c0 = C_lo == 0 ? bs : lower_bound_col(L.b_cols, bs, be, C_lo);
+                Cursor c;
+                c.pos = c0;
+                c.rem = static_cast<int32_t>(be - c0);
+                c.nxt = c0 < be ? __ldg(L.b_cols + c0) : INT_MAX;
+                ws.cur[p] = c;
+            }
+        }
+        __syncwarp();
+        PROF_MARK(0);
         const int64_t row_flops = S.prf ? __ldg(S.prf + i) : 0;
         double ratio = row_flops > 0 ? static_cast<double>(cap) / static_cast<double>(row_flops) : 1.0;
-        bool first = true;
+        int64_t W = imax64(1, static_cast<int64_t>(static_cast<double>(kX) * static_cast<double>(S.k) /
+                                                   fmax(static_cast<double>(cap), 1.0)));
+        int64_t c_lo = C_lo, emitted = 0;
         bool bad = false;
         int replans = 0;
-        while (c_lo < S.k && !bad) {
-            const int64_t c_hi = W >= S.k - c_lo ? S.k : c_lo + W;
-            const bool full = c_lo == 0 && c_hi == S.k;
-            int32_t nk = 0; // this warp's keys in the slab (warp-uniform)
-            if (threadIdx.x == 0)
-                sm.ovf = 0;
-            bool ovf = false;
-            bool replan = false;
-            int64_t slab_products = 0;
-            for (int64_t g0 = 0; g0 < d && !ovf; g0 += kG) {
-                const int ng = static_cast<int>(d - g0 < kG ? d - g0 : kG);
-                PROF_RESET;
-                // ---- runs of this group's A entries in [c_lo, c_hi) ----
-                int64_t s = 0, e = 0;
-                double a = 0.0;
-                if (threadIdx.x < ng) {
-                    const int64_t p = g0 + threadIdx.x;
-                    const int32_t j = __ldg(L.a_cols + abeg + p);
-                    a = __ldg(L.a_vals + abeg + p);
-                    const int64_t bs = __ldg(L.b_rowptr + j), be = __ldg(L.b_rowptr + j + 1);
-                    s = bs + (first ? 0 : cur[p]);
-                    e = full ? be : run_end(L.b_cols, s, be, c_hi);
-                    if (!full)
-                        endr[p] = static_cast<int32_t>(e - bs);
+        while (c_lo < C_hi && !bad) {
+            const int64_t c_hi = W >= C_hi - c_lo ? C_hi : c_lo + W;
+            // ---- plan: runs of every A entry in [c_lo, c_hi), two groups of
+            //      32 entries per step (independent loads in flight) ----
+            int64_t prods = 0;
+            int32_t nr = 0;
+            for (int64_t p0 = 0; p0 < d; p0 += 64) {
+                const int64_t pa = p0 + lane, pb = p0 + 32 + lane;
+                Cursor ca{0, 0, INT_MAX}, cb{0, 0, INT_MAX};
+                if (pa < d)
+                    ca = ws.cur[pa];
+                if (pb < d)
+                    cb = ws.cur[pb];
+                const bool na = ca.nxt < c_hi, nb = cb.nxt < c_hi;
+                bad = bad || (na && ca.nxt < c_lo) || (nb && cb.nxt < c_lo); // an earlier run ended early: unsorted B row
+                int32_t xa = INT_MAX, xb = INT_MAX;
+                int64_t ea = 0, eb = 0;
+                double aa = 0.0, ab = 0.0;
+                if (na) {
+                    aa = __ldg(L.a_vals + abeg + pa);
+                    ea = run_end(L.b_cols, ca.pos, ca.pos + ca.rem, c_hi, &xa);
                 }
-                const int64_t len = e - s;
-                long long tot;
-                const long long packed = block_scan((len << 20) | (len > 0 ? 1 : 0), sm.wsum, &tot);
-                const int32_t nr = static_cast<int32_t>(tot & 0xFFFFF);
-                const int64_t T = tot >> 20;
-                if (len > 0) {
-                    const int ridx = static_cast<int>(packed & 0xFFFFF);
-                    sm.roff[ridx] = static_cast<int32_t>(packed >> 20);
-                    sm.qst[ridx] = s;
-                    sm.av[ridx] = a;
+                if (nb) {
+                    ab = __ldg(L.a_vals + abeg + pb);
+                    eb = run_end(L.b_cols, cb.pos, cb.pos + cb.rem, c_hi, &xb);
                 }
-                if (threadIdx.x == 0)
-                    sm.roff[nr] = static_cast<int32_t>(T);
-                __syncthreads();
-                slab_products += T;
-                if (g0 == 0 && replans < 2) {
-                    // keys this slab will hold, predicted from its products
-                    // (block-uniform): resize before any product is folded
-                    const double est = static_cast<double>(T) * (static_cast<double>(d) / ng) * ratio;
-                    const int64_t w = c_hi - c_lo;
-                    if (est > 1.25 * kXTarget && w > 1) {
-                        W = imax64(1, static_cast<int64_t>(w * (0.9 * kXTarget / est)));
-                        replan = true;
-                    } else if (est < 0.25 * kXTarget && c_hi < S.k) {
-                        W = static_cast<int64_t>(w * min(8.0, 0.5 * kXTarget / fmax(est, 1.0))) + 1;
-                        replan = true;
-                    }
-                    if (replan) {
-                        ++replans;
-                        break;
-                    }
+                const uint32_t Ma = __ballot_sync(kFull, na), Mb = __ballot_sync(kFull, nb);
+                if (na) {
+                    const int r = nr + __popc(Ma & lanemask_lt());
+                    ws.rs[r] = ca.pos;
+                    ws.ra[r] = aa;
+                    ws.rl[r] = static_cast<int32_t>(ea - ca.pos);
+                    ws.rp[r] = static_cast<int32_t>(pa);
+                    ws.rnx[r] = xa;
+                    prods += ea - ca.pos;
                 }
-                PROF_MARK(0);
-                PROF_COUNT(8, 1);
-                PROF_COUNT(9, T);
-                // ---- chunks of kF products: stage, partition by class, fold ----
-                int hint = 0;
-                int32_t col[2];
-                double v[2], va[2]; // B value and A value: multiplied at the scatter, so the
-                                    // prefetched loads are not waited for before the fold
-                auto load = [&](int64_t f0) {
+                nr += __popc(Ma);
+                if (nb) {
+                    const int r = nr + __popc(Mb & lanemask_lt());
+                    ws.rs[r] = cb.pos;
+                    ws.ra[r] = ab;
+                    ws.rl[r] = static_cast<int32_t>(eb - cb.pos);
+                    ws.rp[r] = static_cast<int32_t>(pb);
+                    ws.rnx[r] = xb;
+                    prods += eb - cb.pos;
+                }
+                nr += __popc(Mb);
+            }
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int32_t fw = static_cast<int32_t>(f0) + 64 * warp + 32 * u;
-                        const int32_t f = fw + lane;
-                        col[u] = -1;
-                        v[u] = 0.0;
-                        va[u] = 0.0;
-                        if (fw < T) { // warp-uniform
-                            const int p = find_run(sm.roff, nr, hint, fw, f, lane);
-                            if (f < T) {
-                                const int64_t q = sm.qst[p] + (f - sm.roff[p]);
-                                col[u] = __ldg(L.b_cols + q);
-                                v[u] = __ldg(L.b_vals + q);
-                                va[u] = sm.av[p];
-                            }
-                        }
+            for (int o = 16; o >= 1; o >>= 1)
+                prods += __shfl_xor_sync(kFull, prods, o);
+            if (__any_sync(kFull, bad)) {
+                bad = true;
+                break;
+            }
+            __syncwarp();
+            PROF_MARK(1);
+            if (replans < 2) {
+                // keys this slab will hold, predicted from its products: resize
+                // before any product is folded
+                const double est = static_cast<double>(prods) * ratio;
+                const int64_t w = c_hi - c_lo;
+                bool replan = false;
+                if (est > 1.1 * kX && w > 1) {
+                    W = imax64(1, static_cast<int64_t>(w * (0.85 * kX / est)));
+                    replan = true;
+                } else if (est < 0.25 * kX && c_hi < C_hi) {
+                    W = static_cast<int64_t>(w * fmin(8.0, 0.6 * kX / fmax(est, 1.0))) + 1;
+                    replan = true;
+                }
+                if (replan) {
+                    ++replans;
+                    PROF_COUNT(10, 1);
+                    continue;
+                }
+            }
+            // ---- fold the runs in A order, 32 runs per batch, windows of 32
+            //      products with the next window's loads in flight ----
+            int nk = 0;
+            bool ovf = false, low = false; // low: a column below c_lo (unsorted B row)
+            int64_t nbs = 0;
+            int32_t nbl = 0;
+            double nba = 0.0;
+            if (lane < nr) {
+                nbs = ws.rs[lane];
+                nbl = ws.rl[lane];
+                nba = ws.ra[lane];
+            }
+            for (int32_t r0 = 0; r0 < nr && !ovf; r0 += 32) {
+                const int nb = nr - r0 < 32 ? nr - r0 : 32;
+                const int64_t cb = nbs;
+                const int32_t len = nbl;
+                const double ca = nba;
+                nbs = 0;
+                nbl = 0;
+                nba = 0.0;
+                if (r0 + 32 + lane < nr) { // the next batch's runs
+                    nbs = ws.rs[r0 + 32 + lane];
+                    nbl = ws.rl[r0 + 32 + lane];
+                    nba = ws.ra[r0 + 32 + lane];
+                }
+                int32_t incl = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o)
+                        incl += y;
+                }
+                const int32_t total = __shfl_sync(kFull, incl, 31);
+                const int32_t ce = incl - len; // run start in the batch's flat index
+                int rank = 0;
+                // map window w0 -> (run start, B base, A value) of each lane's product
+                auto load = [&](int32_t w0, int32_t& key, double& bv, double& a, bool& single) {
+                    const uint32_t bit = (lane < nb && ce >= w0 && ce < w0 + 32) ? (1u << (ce - w0)) : 0u;
+                    const uint32_t M = __reduce_or_sync(kFull, bit);
+                    int seg = rank + __popc(M & ((2u << lane) - 1u)) - 1;
+                    seg = seg < 0 ? 0 : (seg > 31 ? 31 : seg);
+                    const int32_t e = __shfl_sync(kFull, ce, seg);
+                    const int64_t base = __shfl_sync(kFull, cb, seg);
+                    a = __shfl_sync(kFull, ca, seg);
+                    rank += __popc(M);
+                    single = M == 0 || M == 1; // every lane in one run: distinct keys
+                    const int32_t t = w0 + lane;
+                    key = -1;
+                    bv = 0.0;
+                    if (t < total) {
+                        key = ldg_keep(L.b_cols + base + (t - e), pol);
+                        bv = ldg_keep(L.b_vals + base + (t - e), pol);
                     }
                 };
-                if (T > 0)
-                    load(0);
-                for (int64_t f0 = 0; f0 < T; f0 += kF) {
-                    // class ranks inside this warp's two windows (stable)
-                    if (lane < kSW)
-                        sm.cnt[warp][lane] = 0;
-                    __syncwarp();
-                    int32_t pos[2], cls[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const bool valid = col[u] >= 0;
-                        if (valid && col[u] < c_lo)
-                            bad = true; // unsorted B row (see header)
-                        cls[u] = valid ? key_class(col[u]) : kSW;
-                        const uint32_t grp = __match_any_sync(kFull, cls[u]);
-                        const int leader = __ffs(grp) - 1;
-                        int32_t base = 0;
-                        if (valid && lane == leader) {
-                            base = sm.cnt[warp][cls[u]];
-                            sm.cnt[warp][cls[u]] = base + __popc(grp);
-                        }
-                        pos[u] = __shfl_sync(kFull, base, leader) + __popc(grp & lanemask_lt());
-                        __syncwarp();
-                    }
-                    __syncthreads(); // (A) counts visible; the previous chunk's folds are done
-                    if (sm.ovf)
+                int32_t key, nkey = -1;
+                double bv, a, nbv = 0.0, na = 0.0;
+                bool single, nsingle = true;
+                load(0, key, bv, a, single);
+                for (int32_t w0 = 0; w0 < total; w0 += 32) {
+                    if (w0 + 32 < total)
+                        load(w0 + 32, nkey, nbv, na, nsingle);
+                    const bool valid = w0 + lane < total;
+                    const double v = __dmul_rn(a, bv);
+                    low = low || (valid && key < c_lo);
+                    if (single)
+                        fold<true>(valid, key, v, tab, nk, lane);
+                    else
+                        fold<false>(valid, key, v, tab, nk, lane);
+                    if (nk > kTWMax) {
                         ovf = true;
-                    if (ovf)
                         break;
-                    // exclusive offsets in (class, staging warp) order: lane l
-                    // holds entries 2l, 2l+1 of the class-major 64-vector
-                    const int t0 = 2 * lane, t1 = 2 * lane + 1;
-                    const int32_t x0 = sm.cnt[t0 & 7][t0 >> 3], x1 = sm.cnt[t1 & 7][t1 >> 3];
-                    int32_t incl = x0 + x1;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int32_t y = __shfl_up_sync(kFull, incl, o);
-                        if (lane >= o)
-                            incl += y;
                     }
-                    const int32_t ex0 = incl - x0 - x1, ex1 = incl - x1;
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        if (col[u] >= 0) {
-                            const int t = cls[u] * kSW + warp;
-                            const int32_t o0 = __shfl_sync(kFull, ex0, t >> 1), o1 = __shfl_sync(kFull, ex1, t >> 1);
-                            const int32_t dst = ((t & 1) ? o1 : o0) + pos[u];
-                            sm.scol[dst] = col[u];
-                            sm.sval[dst] = __dmul_rn(va[u], v[u]);
-                        } else {
-                            __shfl_sync(kFull, ex0, 0);
-                            __shfl_sync(kFull, ex1, 0);
-                        }
-                    }
-                    const int32_t seg_lo = __shfl_sync(kFull, ex0, 4 * warp);
-                    const int32_t seg_hi = warp + 1 < kSW ? __shfl_sync(kFull, ex0, 4 * (warp + 1))
-                                                          : __shfl_sync(kFull, incl, 31);
-                    __syncthreads(); // (C) staging written
-                    PROF_MARK(1);
-                    PROF_COUNT(10, 1);
-                    if (f0 + kF < T)
-                        load(f0 + kF); // next chunk's loads overlap this chunk's folds
-                    // ---- fold class `warp` into partition `warp`, product order ----
-                    for (int32_t x0 = seg_lo; x0 < seg_hi; x0 += 32) {
-                        const bool valid = x0 + lane < seg_hi;
-                        const int32_t key = valid ? sm.scol[x0 + lane] : -1 - lane;
-                        const double val = valid ? sm.sval[x0 + lane] : 0.0;
-                        const uint32_t grp = __match_any_sync(kFull, key);
-                        const bool leader = valid && (__ffs(grp) - 1) == lane;
-                        uint32_t slot = 0;
-                        bool is_new = false;
-                        if (leader) {
-                            slot = key_slot(key);
-                            for (;;) {
-                                const int32_t kx = mykeys[slot];
-                                if (kx == key)
-                                    break;
-                                if (kx == kEmpty) {
-                                    const int32_t old = atomicCAS(&mykeys[slot], kEmpty, key);
-                                    if (old == kEmpty) {
-                                        is_new = true;
-                                        break;
-                                    }
-                                    if (old == key)
-                                        break;
-                                }
-                                slot = (slot + 1) & (kTW - 1);
-                            }
-                        }
-                        double acc = val;
-                        if (leader && !is_new)
-                            acc = __dadd_rn(myvals[slot], val);
-                        uint32_t rest = leader ? (grp & (grp - 1)) : 0u;
-                        const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(rest)));
-                        for (int rr = 0; rr < rounds; ++rr) {
-                            const int src = rest ? __ffs(rest) - 1 : lane;
-                            const double xv = __shfl_sync(kFull, val, src);
-                            if (rest) {
-                                acc = __dadd_rn(acc, xv);
-                                rest &= rest - 1;
-                            }
-                        }
-                        if (leader)
-                            myvals[slot] = acc;
-                        nk += __popc(__ballot_sync(kFull, is_new));
-                        __syncwarp();
-                        if (nk > kTWMax) { // warp-uniform: this slab is too wide
-                            if (lane == 0)
-                                sm.ovf = 1;
-                            break;
-                        }
-                    }
-                    PROF_MARK(5);
+                    key = nkey;
+                    bv = nbv;
+                    a = na;
+                    single = nsingle;
                 }
-                PROF_MARK(2);
-                __syncthreads(); // folds done before the next group's runs overwrite roff/qst/av
-                PROF_MARK(3);
-                if (sm.ovf)
-                    ovf = true;
             }
-            if (replan) {
-                PROF_COUNT(14, 1);
-                continue; // nothing folded, cursors unchanged: plan the slab again
-            }
-            if (__syncthreads_or(bad)) {
-                if (threadIdx.x == 0)
-                    raise_error(L.ctr, kDevUnsorted);
+            PROF_MARK(2);
+            if (__any_sync(kFull, low)) {
                 bad = true;
+                break;
             }
-            PROF_RESET;
-            if (ovf || bad) {
-                PROF_COUNT(11, 1);
-                // abandon the slab: clear the partitions, retry at half width
+            if (ovf) {
+                // abandon the slab: clear the table, retry at half width
                 for (int t = lane; t < kTW; t += 32)
-                    mykeys[t] = kEmpty;
-                __syncthreads();
+                    tab.keys[t] = kEmpty;
+                __syncwarp();
                 W = imax64(1, (c_hi - c_lo) / 2);
+                PROF_COUNT(11, 1);
                 continue;
             }
-            // ---- slab done: advance cursors, emit ----
-            if (!full)
-                for (int64_t p = threadIdx.x; p < d; p += kST)
-                    cur[p] = endr[p];
-            first = false;
-            if (lane == 0)
-                sm.nkeys[warp] = nk;
-            __syncthreads();
-            int32_t before = 0, total = 0;
-#pragma unroll
-            for (int w = 0; w < kSW; ++w) {
-                const int32_t x = sm.nkeys[w];
-                before += w < warp ? x : 0;
-                total += x;
+            // ---- slab done: advance the cursors of the runs, emit ----
+            for (int32_t r = lane; r < nr; r += 32) {
+                const int32_t p = ws.rp[r];
+                Cursor c = ws.cur[p];
+                const int32_t l = ws.rl[r];
+                c.pos += l;
+                c.rem -= l;
+                c.nxt = ws.rnx[r];
+                ws.cur[p] = c;
             }
-            int64_t o = emitted + before;
-            for (int t0 = 0; t0 < kTW; t0 += 32) {
-                const int32_t kx = mykeys[t0 + lane];
-                const bool hit = kx != kEmpty;
-                const uint32_t m = __ballot_sync(kFull, hit);
-                if (hit) {
-                    const int64_t dst = o + __popc(m & lanemask_lt());
-                    if (dst < cap) {
-                        __stcs(L.c_cols + cbase + dst, kx);
-                        __stcs(L.c_vals + cbase + dst, myvals[t0 + lane]);
-                    }
-                    mykeys[t0 + lane] = kEmpty;
+            int64_t base = cbase + emitted;
+            if (parts > 1) {
+                unsigned long long b = 0;
+                if (lane == 0 && nk > 0)
+                    b = atomicAdd(&S.split_out[slot], static_cast<unsigned long long>(nk));
+                base = cbase + static_cast<int64_t>(__shfl_sync(kFull, b, 0));
+            }
+            for (int q = lane; q < nk; q += 32) {
+                const int sl = tab.used[q];
+                const int64_t dst = base + q;
+                if (dst < cbase + cap) {
+                    st_stream(L.c_cols + dst, tab.keys[sl]);
+                    st_stream(L.c_vals + dst, tab.vals[sl]);
                 }
-                o += __popc(m);
+                tab.keys[sl] = kEmpty;
             }
-            emitted += total;
-            PROF_COUNT(12, 1);
-            PROF_COUNT(13, total);
-            // next slab: rescale the width by the density just seen (at most 4x)
+            __syncwarp();
+            emitted += nk;
+            PROF_MARK(3);
+            PROF_COUNT(8, 1);
+            PROF_COUNT(9, prods);
+            // next slab: rescale by the density just seen (at most 4x wider)
             const int64_t w_used = c_hi - c_lo;
-            W = total > 0 ? imax64(1, min(4 * w_used, w_used * kXTarget / total)) : w_used * 4;
-            if (slab_products > 0)
-                ratio = static_cast<double>(total) / static_cast<double>(slab_products);
+            W = nk > 0 ? imax64(1, imin64(4 * w_used, w_used * kX / nk)) : 4 * w_used;
+            if (prods > 0)
+                ratio = static_cast<double>(nk) / static_cast<double>(prods);
             replans = 0;
             c_lo = c_hi;
-            __syncthreads();
-            PROF_MARK(4);
         }
-        if (threadIdx.x == 0 && !bad && emitted != cap)
-            raise_error(L.ctr, emitted < cap ? kDevRowShort : kDevRowOverflow);
+        if (bad) {
+            for (int t = lane; t < kTW; t += 32)
+                tab.keys[t] = kEmpty;
+            __syncwarp();
+            if (lane == 0)
+                raise_error(L.ctr, kDevUnsorted);
+            continue;
+        }
+        if (lane == 0) {
+            if (parts == 1) {
+                if (emitted != cap)
+                    raise_error(L.ctr, emitted < cap ? kDevRowShort : kDevRowOverflow);
+            } else {
+                __threadfence();
+                if (atomicAdd(&S.split_done[slot], 1u) == static_cast<unsigned>(parts - 1)) {
+                    const unsigned long long tot = atomicAdd(&S.split_out[slot], 0ull);
+                    if (static_cast<int64_t>(tot) != cap)
+                        raise_error(L.ctr, static_cast<int64_t>(tot) < cap ? kDevRowShort : kDevRowOverflow);
+                }
+            }
+        }
+        __syncwarp();
     }
 }
 
-size_t slab_smem_bytes() { return sizeof(SlabSmem); }
+// ---------------------------------------------------------------------------
+// work items: heavy rows (largest first), long ones cut into column parts
+// ---------------------------------------------------------------------------
+__global__ void slab_parts_kernel(const int32_t* __restrict__ list, int64_t n, const int64_t* __restrict__ a_rowptr,
+                                  const int64_t* __restrict__ c_rowptr, int64_t k, int64_t* __restrict__ sizes)
+{
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = list[t];
+        const double d = static_cast<double>(a_rowptr[i + 1] - a_rowptr[i]);
+        const double cap = static_cast<double>(c_rowptr[i + 1] - c_rowptr[i]);
+        int64_t P = static_cast<int64_t>(ceil(d * cap / kSplitWork));
+        P = P < 1 ? 1 : (P > 256 ? 256 : P);
+        if (P > k)
+            P = k > 0 ? k : 1;
+        sizes[t + 1] = P; // scanned in place into item offsets
+    }
+}
+
+__global__ void slab_items_kernel(const int32_t* __restrict__ list, int64_t n, const int64_t* __restrict__ item_off,
+                                  int4* __restrict__ items, unsigned long long* split_count)
+{
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = item_off[t];
+        const int32_t P = static_cast<int32_t>(item_off[t + 1] - o);
+        int32_t slot = -1;
+        if (P > 1)
+            slot = static_cast<int32_t>(atomicAdd(split_count, 1ull));
+        for (int32_t q = 0; q < P; ++q)
+            items[o + q] = make_int4(list[t], q, P, slot);
+    }
+}
 
 } // namespace kk
 
@@ -554,27 +606,75 @@ extern "C" int spg_debug_slab_prof(unsigned long long* out, int reset)
 
 namespace kk {
 
-int numeric_slab_blocks_per_sm()
+size_t slab_scratch_per_entry() { return kScratchPerEntry; }
+
+int numeric_slab_warps()
 {
-    const void* fn = reinterpret_cast<const void*>(&numeric_slab_kernel);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SlabSmem));
+    const void* fn = reinterpret_cast<const void*>(&numeric_wslab_kernel);
+    const int smem = static_cast<int>(sizeof(WarpSmem) * kWarps);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kST, sizeof(SlabSmem)) != cudaSuccess)
-        return 1;
-    return b > 0 ? b : 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kWarps * 32, smem) != cudaSuccess || b < 1)
+        b = 1;
+    return b * sm_count() * kWarps;
 }
 
-cudaError_t launch_numeric_slab(const RowLaunch& L, int32_t* scratch, int64_t max_a_row, int64_t k,
-                                const int64_t* prf, int grid, cudaStream_t st)
+int slab_warps_per_cta() { return kWarps; }
+
+// Work items from the sorted heavy-row list.  Pass 1 (items == nullptr):
+// item_off[0..n] = exclusive offsets of each row's parts (item_off[n] =
+// item count).  Pass 2: items[] and the split-row slots.
+cudaError_t build_slab_items(const int32_t* list, int64_t n, const int64_t* a_rowptr, const int64_t* c_rowptr,
+                             int64_t k, int64_t* item_off, int4* items, unsigned long long* split_count,
+                             cudaStream_t st)
 {
-    if (L.nrows <= 0)
+    if (n <= 0)
         return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&numeric_slab_kernel),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SlabSmem));
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 4);
+    if (!items) {
+        cudaError_t e = cudaMemsetAsync(item_off, 0, sizeof(int64_t), st);
+        if (e != cudaSuccess)
+            return e;
+        slab_parts_kernel<<<blocks, 256, 0, st>>>(list, n, a_rowptr, c_rowptr, k, item_off);
+        count_launch();
+        ScanTotals* tot = nullptr;
+        e = cudaMallocAsync(&tot, sizeof(ScanTotals), st);
+        if (e == cudaSuccess)
+            e = cudaMemsetAsync(tot, 0, sizeof(ScanTotals), st);
+        if (e == cudaSuccess)
+            e = scan_sizes_inplace(item_off, n, tot, st); // exclusive offsets, item_off[n] = total
+        if (tot)
+            cudaFreeAsync(tot, st);
+        if (e != cudaSuccess)
+            return e;
+    } else {
+        slab_items_kernel<<<blocks, 256, 0, st>>>(list, n, item_off, items, split_count);
+        count_launch();
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_numeric_slab(const RowLaunch& L, const SlabPlan& P, int64_t k, const int64_t* prf,
+                                cudaStream_t st)
+{
+    if (P.n_items <= 0)
+        return cudaSuccess;
+    const int smem = static_cast<int>(sizeof(WarpSmem) * kWarps);
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&numeric_wslab_kernel),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess)
         return e;
-    SlabArgs S{scratch, max_a_row, k, prf};
-    numeric_slab_kernel<<<grid, kST, sizeof(SlabSmem), st>>>(L, S);
+    if (P.n_split > 0) {
+        e = cudaMemsetAsync(P.split_out, 0, sizeof(unsigned long long) * P.n_split, st);
+        if (e == cudaSuccess)
+            e = cudaMemsetAsync(P.split_done, 0, sizeof(unsigned int) * P.n_split, st);
+        if (e != cudaSuccess)
+            return e;
+    }
+    SlabArgs S{P.items, P.n_items, static_cast<unsigned char*>(P.scratch), P.max_a_row, k, prf, P.split_out,
+               P.split_done};
+    const int grid = static_cast<int>(std::max<int64_t>(1, P.warps / kWarps));
+    numeric_wslab_kernel<<<grid, kWarps * 32, smem, st>>>(L, S);
     count_launch();
     return cudaGetLastError();
 }

@@ -27,9 +27,9 @@ kk.numeric(A, A, h, out=(c.col_indices, c.values))
 e1.record()
 torch.cuda.synchronize()
 f(buf, 0)
-names = ["phase1_cyc", "stage_cyc", "lastfold_cyc", "groupbar_cyc", "emit_cyc", "fold_cyc", "", "",
-         "groups", "products", "chunks", "aborts", "slabs", "keys", "replans", ""]
+names = ["cursor_init_cyc", "plan_cyc", "fold_cyc", "emit_cyc", "", "", "", "",
+         "slabs", "products", "replans", "aborts", "", "", "", ""]
 print(f"s{scale} numeric {e0.elapsed_time(e1):.2f} ms heavy_path={h.heavy_path}")
 for n, v in zip(names, buf):
     if n:
-        print(f"  {n:14s} {v:>16,d}")
+        print(f"  {n:16s} {v:>18,d}")

@@ -1020,3 +1020,98 @@ def test_multiply_host_chunked_values():
         assert np.array_equal(r.c.row_offsets, d.row_offsets)
         assert np.array_equal(r.c.col_indices, d.col_indices)
         assert np.array_equal(r.c.values.view(np.int64), d.values.view(np.int64))
+
+
+# ---------------------------------------------------------------------------
+# full-size configurations checked on ALL rows through per-row canonical
+# digests (spg_row_digests on the device, orc_product_row_digests on the CPU:
+# the same order-independent hash of each row's (column, value bits) set)
+# ---------------------------------------------------------------------------
+def _digest_check(kk, oracle, a, b, c_dev, row_offsets):
+    gd = kk.row_digests(c_dev).cpu().numpy().view(np.uint64)
+    od, osz = oracle.product_row_digests(a, b)
+    assert np.array_equal(np.diff(row_offsets), osz), "row sizes differ"
+    bad = np.nonzero(gd != od)[0]
+    assert bad.size == 0, f"{bad.size} rows differ (first {bad[:5].tolist()})"
+
+
+def test_row_digests_match_oracle_small(kk, oracle):
+    rng = np.random.default_rng(43)
+    a = random_csr(rng, 200, 150, 0.1, shuffle=True)
+    b = random_csr(rng, 150, 170, 0.1, shuffle=True)
+    res = kk.multiply(a, b)
+    c = res.c.to_host()
+    assert np.array_equal(kk.row_digests(res.c).cpu().numpy().view(np.uint64), oracle.row_digests(c))
+    _digest_check(kk, oracle, a, b, res.c, c.row_offsets)
+    # a permuted row has the digest of its sorted form; one flipped value bit does not
+    sc, sv = oracle.sort_rows(c.row_offsets, c.col_indices, c.values)
+    s = kk.CsrMatrix(c.num_rows, c.num_cols, c.row_offsets, sc, sv, True)
+    assert np.array_equal(oracle.row_digests(s), oracle.row_digests(c))
+    sv2 = sv.copy()
+    sv2.view(np.int64)[3] ^= 1
+    s2 = kk.CsrMatrix(c.num_rows, c.num_cols, c.row_offsets, sc, sv2, True)
+    assert (oracle.row_digests(s2) != oracle.row_digests(c)).sum() == 1
+
+
+def test_c2_full_size_all_rows(kk, oracle):
+    """Config 2 (160^3, 2.9 G products): every row of C against the oracle."""
+    from paper_1801_03065_b200 import generators as G
+    a = G.laplace3d(160)
+    res = kk.multiply(a, a)
+    _digest_check(kk, oracle, a, a, res.c, res.handle.c_row_offsets)
+
+
+def test_c5_reuse_passes_all_rows(kk, oracle):
+    """Config 5 (200^3): one symbolic, numeric passes with perturbed values;
+    pass 1 (hashing kernels) and pass 3 (slot replay) checked on every row."""
+    import torch
+    from paper_1801_03065_b200 import generators as G
+    a = G.laplace3d(200)
+    da = a.to_device()
+    h = kk.symbolic(da, da)
+    rng = np.random.default_rng(5)
+    base = a.values.copy()
+    ro = h.c_row_offsets
+    for p in range(3):
+        a.values[:] = base * (1.0 + 1e-3 * rng.uniform(-1.0, 1.0, base.shape))
+        da.values.copy_(torch.from_numpy(a.values))
+        c = kk.numeric(da, da, h)
+        if p in (0, 2):
+            _digest_check(kk, oracle, a, a, c, ro)
+        del c
+    assert h.replay_state == 2
+
+
+def test_c4_rmat_s20_all_rows(kk, oracle):
+    """Config 4 at its BASELINE size (R-MAT scale 20: 20.9 G products, C =
+    9.71 G entries / 116.5 GB on the device): every row against the oracle,
+    plus SURVEY §8c's row sample (every 64th row and the 1,024 heaviest)
+    compared entry by entry (sorted columns, value bits)."""
+    import torch
+    from paper_1801_03065_b200 import generators as G
+    a = G.rmat(20, 16, 1)
+    da = a.to_device()
+    h = kk.symbolic(da, da)
+    assert h.flops.total_flops == 20_938_949_470 and h.nnz_c() == 9_711_687_861
+    assert h.max_row_size == 484_845 and h.heavy_path == 2
+    c = kk.numeric(da, da, h, kk.PhaseStats())
+    ro = h.c_row_offsets
+    _digest_check(kk, oracle, a, a, c, ro)
+    sizes = np.diff(ro)
+    rows = np.unique(np.concatenate([np.arange(0, a.num_rows, 64), np.argsort(sizes, kind="stable")[-1024:]]))
+    rows = rows[sizes[rows] > 0]
+    lo, hi = ro[rows], ro[rows + 1]
+    idx = torch.from_numpy(np.concatenate([np.arange(x, y) for x, y in zip(lo, hi)])).to(c.values.device)
+    gc = c.col_indices.index_select(0, idx).cpu().numpy()
+    gv = c.values.index_select(0, idx).cpu().numpy()
+    del c
+    torch.cuda.empty_cache()
+    samp = _row_sample(kk, a, rows)
+    oro, ocols, ovals = oracle.multiply(samp, a)
+    assert np.array_equal(np.diff(oro), sizes[rows])
+    sro = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(sizes[rows], out=sro[1:])
+    sc, sv = oracle.sort_rows(oro, ocols, ovals)
+    tc, tv = oracle.sort_rows(sro, gc, gv)
+    assert np.array_equal(sc, tc)
+    assert np.array_equal(sv.view(np.int64), tv.view(np.int64))
