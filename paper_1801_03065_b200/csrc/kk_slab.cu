@@ -62,36 +62,42 @@ __device__ __forceinline__ uint32_t key_slot(int32_t key)
     return (static_cast<uint32_t>(key) * 0x9E3779B1u) >> 22; // 10 bits
 }
 
-// First q in [s, be) with cols[q] >= c, for a column-sorted row; *at = cols[q]
-// (INT_MAX when q == be).  Runs are mostly short: eight independent loads
-// first, then a galloping search.
-__device__ __forceinline__ int64_t run_end(const int32_t* __restrict__ cols, int64_t s, int64_t be, int64_t c,
-                                           int32_t* at)
+// Run-end search, split so that two A entries' first loads are in flight
+// together: probe16 loads the 16 columns at q (INT_MAX past be), finish16
+// evaluates them and, for a run longer than 16, gallops.  Returns the first
+// q in [s, be) with cols[q] >= c (column-sorted row) and *at = cols[q]
+// (INT_MAX when q == be).
+struct Probe16 {
+    int32_t v[16];
+};
+
+__device__ __forceinline__ void probe16(const int32_t* __restrict__ cols, int64_t q, int64_t be, Probe16& P)
 {
-    int64_t q = s;
-    for (int round = 0; round < 2; ++round) {
-        const int64_t n = be - q;
-        if (n <= 0) {
-            *at = INT_MAX;
-            return be;
-        }
-        int32_t v[8];
+    const int64_t n = be - q;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-            v[u] = u < n ? __ldg(cols + q + u) : INT_MAX;
-        int first = 8;
-        int32_t fv = INT_MAX;
+    for (int u = 0; u < 16; ++u)
+        P.v[u] = u < n ? __ldg(cols + q + u) : INT_MAX;
+}
+
+__device__ __forceinline__ int64_t finish16(const int32_t* __restrict__ cols, int64_t q, int64_t be, int64_t c,
+                                            const Probe16& P, int32_t* at)
+{
+    int first = 16;
+    int32_t fv = INT_MAX;
 #pragma unroll
-        for (int u = 7; u >= 0; --u)
-            if (v[u] >= c) {
-                first = u;
-                fv = v[u];
-            }
-        if (first < 8) {
-            *at = fv;
-            return q + first;
+    for (int u = 15; u >= 0; --u)
+        if (P.v[u] >= c) {
+            first = u;
+            fv = P.v[u];
         }
-        q += 8;
+    if (first < 16) {
+        *at = fv;
+        return q + first < be ? q + first : be;
+    }
+    q += 16;
+    if (q >= be) {
+        *at = INT_MAX;
+        return be;
     }
     // gallop: cols[q - 1] < c
     int64_t step = 16, lo = q - 1, hi = be;
@@ -339,14 +345,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const Row
                 int32_t xa = INT_MAX, xb = INT_MAX;
                 int64_t ea = 0, eb = 0;
                 double aa = 0.0, ab = 0.0;
-                if (na) {
+                Probe16 Pa, Pb; // both groups' first loads in flight before either is evaluated
+                probe16(L.b_cols, ca.pos, na ? ca.pos + ca.rem : ca.pos, Pa);
+                probe16(L.b_cols, cb.pos, nb ? cb.pos + cb.rem : cb.pos, Pb);
+                if (na)
                     aa = __ldg(L.a_vals + abeg + pa);
-                    ea = run_end(L.b_cols, ca.pos, ca.pos + ca.rem, c_hi, &xa);
-                }
-                if (nb) {
+                if (nb)
                     ab = __ldg(L.a_vals + abeg + pb);
-                    eb = run_end(L.b_cols, cb.pos, cb.pos + cb.rem, c_hi, &xb);
-                }
+                if (na)
+                    ea = finish16(L.b_cols, ca.pos, ca.pos + ca.rem, c_hi, Pa, &xa);
+                if (nb)
+                    eb = finish16(L.b_cols, cb.pos, cb.pos + cb.rem, c_hi, Pb, &xb);
                 const uint32_t Ma = __ballot_sync(kFull, na), Mb = __ballot_sync(kFull, nb);
                 if (na) {
                     const int r = nr + __popc(Ma & lanemask_lt());
@@ -384,10 +393,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const Row
                 const double est = static_cast<double>(prods) * ratio;
                 const int64_t w = c_hi - c_lo;
                 bool replan = false;
-                if (est > 1.1 * kX && w > 1) {
-                    W = imax64(1, static_cast<int64_t>(w * (0.85 * kX / est)));
+                if (est > 1.15 * kX && w > 1) {
+                    W = imax64(1, static_cast<int64_t>(w * (0.9 * kX / est)));
                     replan = true;
-                } else if (est < 0.25 * kX && c_hi < C_hi) {
+                } else if (est < 0.2 * kX && c_hi < C_hi) {
                     W = static_cast<int64_t>(w * fmin(8.0, 0.6 * kX / fmax(est, 1.0))) + 1;
                     replan = true;
                 }
@@ -397,68 +406,88 @@ __global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const Row
                     continue;
                 }
             }
-            // ---- fold the runs in A order, 32 runs per batch, windows of 32
-            //      products with the next window's loads in flight ----
+            // ---- fold the runs in A order: batches of 32 runs, windows of 32
+            //      products; the next window's loads (across batch boundaries)
+            //      are in flight while a window folds ----
             int nk = 0;
             bool ovf = false, low = false; // low: a column below c_lo (unsorted B row)
-            int64_t nbs = 0;
-            int32_t nbl = 0;
-            double nba = 0.0;
-            if (lane < nr) {
-                nbs = ws.rs[lane];
-                nbl = ws.rl[lane];
-                nba = ws.ra[lane];
-            }
-            for (int32_t r0 = 0; r0 < nr && !ovf; r0 += 32) {
-                const int nb = nr - r0 < 32 ? nr - r0 : 32;
-                const int64_t cb = nbs;
-                const int32_t len = nbl;
-                const double ca = nba;
-                nbs = 0;
-                nbl = 0;
-                nba = 0.0;
-                if (r0 + 32 + lane < nr) { // the next batch's runs
-                    nbs = ws.rs[r0 + 32 + lane];
-                    nbl = ws.rl[r0 + 32 + lane];
-                    nba = ws.ra[r0 + 32 + lane];
+            struct Batch {
+                int64_t cb; // this lane's run: B start
+                double ca;  //                A value
+                int32_t ce; //                start in the batch's flat index
+                int32_t total, nb, rank;
+            };
+            auto fetch = [&](int32_t r0, int64_t& s0, int32_t& l0, double& a0) {
+                s0 = 0;
+                l0 = 0;
+                a0 = 0.0;
+                if (r0 + lane < nr) {
+                    s0 = ws.rs[r0 + lane];
+                    l0 = ws.rl[r0 + lane];
+                    a0 = ws.ra[r0 + lane];
                 }
-                int32_t incl = len;
+            };
+            auto make = [&](int32_t r0, int64_t s0, int32_t l0, double a0) {
+                Batch B;
+                int32_t incl = l0;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int32_t y = __shfl_up_sync(kFull, incl, o);
                     if (lane >= o)
                         incl += y;
                 }
-                const int32_t total = __shfl_sync(kFull, incl, 31);
-                const int32_t ce = incl - len; // run start in the batch's flat index
-                int rank = 0;
-                // map window w0 -> (run start, B base, A value) of each lane's product
-                auto load = [&](int32_t w0, int32_t& key, double& bv, double& a, bool& single) {
-                    const uint32_t bit = (lane < nb && ce >= w0 && ce < w0 + 32) ? (1u << (ce - w0)) : 0u;
-                    const uint32_t M = __reduce_or_sync(kFull, bit);
-                    int seg = rank + __popc(M & ((2u << lane) - 1u)) - 1;
-                    seg = seg < 0 ? 0 : (seg > 31 ? 31 : seg);
-                    const int32_t e = __shfl_sync(kFull, ce, seg);
-                    const int64_t base = __shfl_sync(kFull, cb, seg);
-                    a = __shfl_sync(kFull, ca, seg);
-                    rank += __popc(M);
-                    single = M == 0 || M == 1; // every lane in one run: distinct keys
-                    const int32_t t = w0 + lane;
-                    key = -1;
-                    bv = 0.0;
-                    if (t < total) {
-                        key = ldg_keep(L.b_cols + base + (t - e), pol);
-                        bv = ldg_keep(L.b_vals + base + (t - e), pol);
-                    }
-                };
+                B.cb = s0;
+                B.ca = a0;
+                B.ce = incl - l0;
+                B.total = __shfl_sync(kFull, incl, 31);
+                B.nb = nr - r0 < 32 ? nr - r0 : 32;
+                B.rank = 0;
+                return B;
+            };
+            // window w0 of batch B -> this lane's (key, B value, A value)
+            auto map = [&](Batch& B, int32_t w0, int32_t& key, double& bv, double& a, bool& single) {
+                const uint32_t bit = (lane < B.nb && B.ce >= w0 && B.ce < w0 + 32) ? (1u << (B.ce - w0)) : 0u;
+                const uint32_t M = __reduce_or_sync(kFull, bit);
+                int seg = B.rank + __popc(M & ((2u << lane) - 1u)) - 1;
+                seg = seg < 0 ? 0 : (seg > 31 ? 31 : seg);
+                const int32_t e = __shfl_sync(kFull, B.ce, seg);
+                const int64_t base = __shfl_sync(kFull, B.cb, seg);
+                a = __shfl_sync(kFull, B.ca, seg);
+                B.rank += __popc(M);
+                single = M == 0 || M == 1; // every lane in one run: distinct keys
+                const int32_t t = w0 + lane;
+                key = -1;
+                bv = 0.0;
+                if (t < B.total) {
+                    key = ldg_keep(L.b_cols + base + (t - e), pol);
+                    bv = ldg_keep(L.b_vals + base + (t - e), pol);
+                }
+            };
+            if (nr > 0) {
+                int64_t s0, s1, s2;
+                int32_t l0, l1, l2;
+                double a0, a1, a2;
+                fetch(0, s0, l0, a0);
+                fetch(32, s1, l1, a1);
+                fetch(64, s2, l2, a2);
+                Batch cur = make(0, s0, l0, a0);
+                Batch nxt = make(32, s1, l1, a1);
+                int32_t cr0 = 0, cw0 = 0;
                 int32_t key, nkey = -1;
                 double bv, a, nbv = 0.0, na = 0.0;
                 bool single, nsingle = true;
-                load(0, key, bv, a, single);
-                for (int32_t w0 = 0; w0 < total; w0 += 32) {
-                    if (w0 + 32 < total)
-                        load(w0 + 32, nkey, nbv, na, nsingle);
-                    const bool valid = w0 + lane < total;
+                map(cur, 0, key, bv, a, single);
+                for (;;) {
+                    bool next_in_cur = false, has_next = true;
+                    if (cw0 + 32 < cur.total) {
+                        map(cur, cw0 + 32, nkey, nbv, na, nsingle);
+                        next_in_cur = true;
+                    } else if (cr0 + 32 < nr) {
+                        map(nxt, 0, nkey, nbv, na, nsingle);
+                    } else {
+                        has_next = false;
+                    }
+                    const bool valid = cw0 + lane < cur.total;
                     const double v = __dmul_rn(a, bv);
                     low = low || (valid && key < c_lo);
                     if (single)
@@ -468,6 +497,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const Row
                     if (nk > kTWMax) {
                         ovf = true;
                         break;
+                    }
+                    if (!has_next)
+                        break;
+                    if (next_in_cur) {
+                        cw0 += 32;
+                    } else {
+                        cr0 += 32;
+                        cw0 = 0;
+                        cur = nxt; // its window 0 is already mapped (rank advanced)
+                        nxt = make(cr0 + 32, s2, l2, a2);
+                        fetch(cr0 + 64, s2, l2, a2);
                     }
                     key = nkey;
                     bv = nbv;
