@@ -89,9 +89,12 @@ __global__ void __launch_bounds__(256) fingerprint_kernel(int64_t rows, const in
     uint64_t w = fp_weight(h + 4 * tid);
     const uint64_t wstep = 4ull * static_cast<uint64_t>(stride) * kFpK2;
     for (int64_t q = tid; q < nvec; q += stride, w += wstep) {
+        // two adjacent columns per mixed term (the weight is the first one's):
+        // still an injective (position, value) input, half the mixing work
         const int4 x = __ldg(v + q);
-        acc += fp_term(w, static_cast<uint32_t>(x.x)) + fp_term(w + kFpK2, static_cast<uint32_t>(x.y))
-            + fp_term(w + 2 * kFpK2, static_cast<uint32_t>(x.z)) + fp_term(w + 3 * kFpK2, static_cast<uint32_t>(x.w));
+        acc += fp_term(w, static_cast<uint32_t>(x.x) | (static_cast<uint64_t>(static_cast<uint32_t>(x.y)) << 32))
+            + fp_term(w + 2 * kFpK2,
+                      static_cast<uint32_t>(x.z) | (static_cast<uint64_t>(static_cast<uint32_t>(x.w)) << 32));
     }
     for (int64_t q = h + 4 * nvec + tid; q < nnz; q += stride)
         acc += fp_term(fp_weight(q), static_cast<uint32_t>(__ldg(c + q)));
