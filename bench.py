@@ -85,6 +85,13 @@ def workload(cfg: int, scale: float, gen):
     return mats, wl
 
 
+def operand_a(cfg: int, scale: float = 1.0):
+    """(A, label) of a config from the product generators (profiling scripts)."""
+    from paper_1801_03065_b200 import generators as G
+    mats, wl = workload(cfg, scale, G)
+    return mats["A"], wl
+
+
 def products(cfg: int, mats):
     """The (A, B) pairs one step multiplies."""
     if cfg == 3:
@@ -542,6 +549,9 @@ def run_aa(args, kk, mats, dev, timer, barrier):
     }
     # ---- end to end through the host API (pinned host CSR in, host C out) ----
     if not args.no_e2e:
+        del cols, vals, h0  # the host path allocates its own device C (c4: 116.5 GB)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         res["e2e"] = e2e_multiply_host(args, kk, a_host, nnz_c, dev, barrier, stream=timer.stream)
     return res
 

@@ -26,6 +26,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -61,11 +62,35 @@ void cuda(cudaError_t e)
         throw SpgemmError(std::string("CUDA: ") + cudaGetErrorString(e));
 }
 
+// host memcpy split over the host's cores (a single thread moves ~5-10 GB/s,
+// well below the host link)
+void par_copy(void* dst, const void* src, size_t n)
+{
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (n < (size_t{4} << 20) || hw == 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t per = (n + hw - 1) / hw;
+    for (unsigned t = 1; t < hw; ++t) {
+        const size_t off = per * t;
+        if (off >= n)
+            break;
+        th.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, std::min(per, n - off));
+        });
+    }
+    std::memcpy(dst, src, std::min(per, n));
+    for (auto& x : th)
+        x.join();
+}
+
 // pinned staging: host vectors are pageable, so copies go through a pinned
-// bounce buffer in chunks, the host memcpy of chunk i+1 overlapping the DMA
-// of chunk i
+// bounce buffer in chunks, the (multi-threaded) host copy of chunk i+1
+// overlapping the DMA of chunk i
 struct Staging {
-    static constexpr size_t kChunk = size_t{32} << 20;
+    static constexpr size_t kChunk = size_t{64} << 20;
     void* buf[2] = {nullptr, nullptr};
     cudaEvent_t done[2] = {nullptr, nullptr};
     Staging()
@@ -94,7 +119,7 @@ struct Staging {
         for (size_t off = 0, q = 0; off < bytes; off += kChunk, q ^= 1) {
             const size_t n = bytes - off < kChunk ? bytes - off : kChunk;
             cuda(cudaEventSynchronize(done[q])); // the buffer's previous DMA has drained
-            std::memcpy(buf[q], s + off, n);
+            par_copy(buf[q], s + off, n);
             cuda(cudaMemcpyAsync(d + off, buf[q], n, cudaMemcpyHostToDevice, st));
             cuda(cudaEventRecord(done[q], st));
         }
@@ -108,7 +133,7 @@ struct Staging {
         auto drain = [&](int q) {
             if (pend_n[q]) {
                 cuda(cudaEventSynchronize(done[q]));
-                std::memcpy(d + pend_off[q], buf[q], pend_n[q]);
+                par_copy(d + pend_off[q], buf[q], pend_n[q]);
                 pend_n[q] = 0;
             }
         };
@@ -470,6 +495,26 @@ CsrMatrix numeric_impl(const CsrMatrix& a, const CsrMatrix& b, const SpgemmHandl
         || a.nnz() != handle.nnz_a || b.nnz() != handle.nnz_b)
         throw ReuseError("numeric: operands do not match the symbolic handle");
 
+    // C's owning vectors are value-initialised by resize (the reference's
+    // NumericSink pays the same zero-fill, engine.cpp:456-461): done on two
+    // threads while the operands upload and the GPU computes
+    const int64_t nnz = handle.nnz_c();
+    CsrMatrix c;
+    c.num_rows = handle.m;
+    c.num_cols = handle.k;
+    std::thread fill_c([&] { c.col_indices.resize(static_cast<size_t>(nnz)); });
+    std::thread fill_v([&] { c.values.resize(static_cast<size_t>(nnz)); });
+    struct Join {
+        std::thread& a;
+        std::thread& b;
+        ~Join()
+        {
+            if (a.joinable())
+                a.join();
+            if (b.joinable())
+                b.join();
+        }
+    } join{fill_c, fill_v};
     Cache& cache = Cache::get();
     std::lock_guard<std::mutex> lk(cache.mu);
     const uint64_t dig = handle_digest(handle);
@@ -484,7 +529,6 @@ CsrMatrix numeric_impl(const CsrMatrix& a, const CsrMatrix& b, const SpgemmHandl
     if (!(same_call && e->fresh_a == &a && e->fresh_b == &b))
         e->upload(a, b);
     e->fresh_a = e->fresh_b = nullptr;
-    const int64_t nnz = handle.nnz_c();
     const size_t need = static_cast<size_t>(nnz > 0 ? nnz : 1);
     if (need > e->cap_c) {
         cudaFree(e->dc);
@@ -497,12 +541,9 @@ CsrMatrix numeric_impl(const CsrMatrix& a, const CsrMatrix& b, const SpgemmHandl
     }
     spg_phase_stats st{};
     check(spg_numeric(e->h, &e->a.view, e->bview(), e->dc, e->dv, stats ? &st : nullptr, nullptr));
-    CsrMatrix c;
-    c.num_rows = handle.m;
-    c.num_cols = handle.k;
     c.row_offsets = handle.c_row_offsets;
-    c.col_indices.resize(static_cast<size_t>(nnz));
-    c.values.resize(static_cast<size_t>(nnz));
+    fill_c.join();
+    fill_v.join();
     if (nnz > 0) {
         e->stg->down(c.col_indices.data(), e->dc, sizeof(int32_t) * nnz, nullptr);
         e->stg->down(c.values.data(), e->dv, sizeof(double) * nnz, nullptr);

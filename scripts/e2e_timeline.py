@@ -5,7 +5,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from bench import workload  # noqa: E402
+from bench import operand_a as workload  # noqa: E402
 from paper_1801_03065_b200 import host  # noqa: E402
 
 cfg_id, scale = int(sys.argv[1]), float(sys.argv[2])

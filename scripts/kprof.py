@@ -10,13 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_1801_03065_b200 as kk  # noqa: E402
-from bench import workload as _wl
-from paper_1801_03065_b200 import generators as _G
-
-
-def workload(c, s):
-    m, wl = _wl(c, s, _G)
-    return m["A"], wl  # noqa: E402
+from bench import operand_a as workload  # noqa: E402
 
 
 def main():

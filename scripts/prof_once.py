@@ -4,13 +4,7 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1801_03065_b200 as kk
-from bench import workload as _wl
-from paper_1801_03065_b200 import generators as _G
-
-
-def workload(c, s):
-    m, wl = _wl(c, s, _G)
-    return m["A"], wl
+from bench import operand_a as workload  # noqa: E402
 cfg_id, scale = int(sys.argv[1]), float(sys.argv[2])
 a, wl = workload(cfg_id, scale)
 A = a.to_device()

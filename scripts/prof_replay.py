@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_1801_03065_b200 as kk  # noqa: E402
-from bench import workload  # noqa: E402
+from bench import operand_a as workload  # noqa: E402
 
 cfg_id, scale = int(sys.argv[1]), float(sys.argv[2])
 a, wl = workload(cfg_id, scale)

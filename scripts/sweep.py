@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 os.environ.setdefault("KK_NO_REPLAY", "1")  # time the hashing kernels (bench.py times the replay)
 import paper_1801_03065_b200 as kk
-from bench import workload
+from bench import operand_a as workload
 
 cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0

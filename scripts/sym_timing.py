@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_1801_03065_b200 as kk  # noqa: E402
-from bench import workload  # noqa: E402
+from bench import operand_a as workload  # noqa: E402
 
 a, _ = workload(2, 1.0)
 A = a.to_device()
