@@ -567,9 +567,9 @@ def e2e_multiply_host(args, kk, a_host, nnz_c, dev, barrier, stream, a_rows=None
         avail = psutil.virtual_memory().available
     except Exception:
         avail = None
-    if avail is not None and need > 0.6 * avail:
+    if avail is not None and need > 0.35 * avail:
         return {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
-                "unavailable": f"C plus inputs ({need / 1e9:.1f} GB) exceed 60% of this host's available "
+                "unavailable": f"C plus inputs ({need / 1e9:.1f} GB) exceed 35% of this host's available "
                                f"memory ({avail / 1e9:.1f} GB) for pinned buffers"}
     pa = host.PinnedCsr.from_csr(a_host)
     outbuf = (torch.empty(m + 1, dtype=torch.int64).pin_memory(),

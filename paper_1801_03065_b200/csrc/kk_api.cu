@@ -984,62 +984,51 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         int64_t* d_prcf = dalloc<int64_t>(std::max(m, 1), st, "per-row cflops");
         int32_t* d_csize = dalloc<int32_t>(std::max(n, 1), st, "csize");
         // B slots hold the compressed pairs; index them like B (base-relative)
-        int64_t bview[2] = {0, 0}, aview[2] = {0, 0};
         int2* d_cp_alloc = dalloc<int2>(std::max<int64_t>(b->nnz, 1), st, "compressed pairs");
         Totals* d_tot = dalloc<Totals>(1, st, "totals");
         ScanTotals* d_stot = dalloc<ScanTotals>(1, st, "scan totals");
 
-        int* d_crange = dalloc<int>(2, st, "column range");
         PinnedBuf pin(sizeof(Totals) + sizeof(ScanTotals) + sizeof(DevCounters) + 64 + 16);
         auto* htot = static_cast<Totals*>(pin.p);
         auto* hstot = reinterpret_cast<ScanTotals*>(htot + 1);
         auto* hctr = reinterpret_cast<DevCounters*>(hstot + 1);
         auto* hviews = reinterpret_cast<int64_t*>(hctr + 1);
 
+        // the view offsets are read back with the flop totals (one host round
+        // trip): the kernels rebase the compressed pairs on B's first offset
+        // themselves, and compress only the band of B rows a row shard of A
+        // references (A at most half as tall as B) from a device-side range
         cuda_check(cudaMemcpyAsync(hviews + 0, a->row_offsets, 8, cudaMemcpyDeviceToHost, st), "A view");
         cuda_check(cudaMemcpyAsync(hviews + 1, a->row_offsets + m, 8, cudaMemcpyDeviceToHost, st), "A view");
         cuda_check(cudaMemcpyAsync(hviews + 2, b->row_offsets, 8, cudaMemcpyDeviceToHost, st), "B view");
         cuda_check(cudaMemcpyAsync(hviews + 3, b->row_offsets + n, 8, cudaMemcpyDeviceToHost, st), "B view");
-        // the band of B rows A references, when A is at most half as tall as
-        // B (a row shard): only that band is compressed
-        int* hcrange = reinterpret_cast<int*>(hviews + 8);
-        hcrange[0] = 0;
-        hcrange[1] = n - 1;
+        int* d_crange = nullptr;
         if (int64_t{m} * 2 <= n) {
+            d_crange = dalloc<int>(2, st, "column range");
             cuda_check(launch_col_range(m, a->row_offsets, a->col_indices, d_crange, st), "column range");
-            cuda_check(cudaMemcpyAsync(hcrange, d_crange, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "column range");
         }
         cuda_check(cudaEventRecord(ev[0], st), "event");
         cuda_check(cudaMemsetAsync(d_tot, 0, sizeof(Totals), st), "memset");
         cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");
         cuda_check(cudaMemsetAsync(h->d_ctr, 0, sizeof(DevCounters), st), "memset");
-        cuda_check(cudaStreamSynchronize(st), "views");
-        aview[0] = hviews[0];
-        aview[1] = hviews[1];
-        bview[0] = hviews[2];
-        bview[1] = hviews[3];
-        if (aview[1] - aview[0] != a->nnz || bview[1] - bview[0] != b->nnz)
-            fail(SPG_ERR_CONTRACT, "symbolic: nnz does not match row_offsets");
-        int2* d_cp = d_cp_alloc - bview[0];
+        int2* d_cp = d_cp_alloc; // rebased on the device (cpair_of)
 
         // ---- K3 + K1/K4 ----
-        const int32_t j0 = std::clamp(hcrange[0], 0, n), j1 = std::clamp(hcrange[1] + 1, j0, n);
-        cudaFreeAsync(d_crange, st);
-        cuda_check(launch_compress(j1 - j0, b->row_offsets + j0, b->col_indices, d_csize + j0, d_cp, &d_tot->nnz_bc,
-                                   &d_tot->unsorted, st),
+        cuda_check(launch_compress(n, b->row_offsets, b->col_indices, d_csize, d_cp_alloc, &d_tot->nnz_bc,
+                                   &d_tot->unsorted, d_crange, st),
                    "compress");
+        if (d_crange)
+            cudaFreeAsync(d_crange, st);
         const double avg_len = m > 0 ? static_cast<double>(a->nnz) / m : 0.0;
         cuda_check(launch_flops(m, avg_len, a->row_offsets, a->col_indices, b->row_offsets, d_csize,
                                 h->d_prf, d_prcf, d_tot, st),
                    "flops");
-        // longest A row (cursor arrays of the column-slab kernel)
-        cuda_check(launch_row_bucket_hist(m, a->row_offsets, d_stot, st), "A row lengths");
         cuda_check(cudaMemcpyAsync(htot, d_tot, sizeof(Totals), cudaMemcpyDeviceToHost, st), "totals");
-        cuda_check(cudaMemcpyAsync(hstot, d_stot, sizeof(ScanTotals), cudaMemcpyDeviceToHost, st), "A totals");
-        cuda_check(cudaMemsetAsync(d_stot, 0, sizeof(ScanTotals), st), "memset");
         cuda_check(cudaEventRecord(ev[1], st), "event");
         cuda_check(cudaStreamSynchronize(st), "flops sync");
-        h->max_a_row = static_cast<int64_t>(hstot->max_size);
+        if (hviews[1] - hviews[0] != a->nnz || hviews[3] - hviews[2] != b->nnz)
+            fail(SPG_ERR_CONTRACT, "symbolic: nnz does not match row_offsets");
+        h->max_a_row = static_cast<int64_t>(htot->max_alen);
         h->b_sorted = htot->unsorted == 0;
 
         // ---- host decisions (engine.cpp:409-423, compression.cpp:118-147) ----

@@ -589,6 +589,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
+    const int2* __restrict__ cpair = cpair_of(L);
     unsigned char* region = smem + (size_t)wib * L.lay.bytes;
     int32_t* keys = reinterpret_cast<int32_t*>(region + L.lay.off_ids);
     uint32_t* words = reinterpret_cast<uint32_t*>(region + L.lay.off_map);
@@ -646,7 +647,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
             };
             auto load = [&](int64_t q, int32_t& key, uint32_t& word) {
                 if constexpr (kCompressed) {
-                    const int2 pr = __ldg(L.cpair + q);
+                    const int2 pr = __ldg(cpair + q);
                     key = pr.x;
                     word = static_cast<uint32_t>(pr.y);
                 } else {

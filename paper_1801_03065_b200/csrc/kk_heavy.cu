@@ -77,6 +77,7 @@ struct HMap {
 template <bool kNumeric, bool kCompressed, class F>
 __device__ __forceinline__ void walk_products(const RowLaunch& L, int64_t p_lo, int64_t p_hi, int lane, F&& fn)
 {
+    const int2* __restrict__ cpair = kCompressed ? cpair_of(L) : nullptr;
     for (int64_t p0 = p_lo; p0 < p_hi; p0 += 32) {
         const int na = static_cast<int>(p_hi - p0 < 32 ? p_hi - p0 : 32);
         int64_t bb = 0;
@@ -108,7 +109,7 @@ __device__ __forceinline__ void walk_products(const RowLaunch& L, int64_t p_lo, 
             if (t < fm.total) {
                 const int64_t q = base + (t - e);
                 if constexpr (kCompressed) {
-                    const int2 pr = __ldg(L.cpair + q);
+                    const int2 pr = __ldg(cpair + q);
                     key = pr.x;
                     word = static_cast<uint32_t>(pr.y);
                 } else {
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L,
     uint32_t* sm = bm + words;
     __shared__ unsigned long long red[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int2* __restrict__ cpair = kCompressed ? cpair_of(L) : nullptr;
     for (int t = threadIdx.x; t < words + swords; t += blockDim.x)
         bm[t] = 0u;
     __syncthreads();
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L,
                 if (t < tot) {
                     const int64_t q = base + (t - e);
                     if constexpr (kCompressed) {
-                        const int2 pr = __ldg(L.cpair + q);
+                        const int2 pr = __ldg(cpair + q);
                         add(pr.x, static_cast<uint32_t>(pr.y));
                     } else {
                         const int32_t key = __ldg(L.b_cols + q);

@@ -31,6 +31,7 @@ struct Totals {
     unsigned long long total_f, max_f, total_cf, max_cf;
     unsigned long long nnz_bc; // compressed pairs written (the compress pass)
     unsigned long long unsorted; // > 0: some compressed B row is not strictly column-sorted
+    unsigned long long max_alen; // longest A row (cursor arrays of the column-slab kernel)
     unsigned long long hist_f[64];
     unsigned long long hist_cf[64];
 };
@@ -57,7 +58,8 @@ struct RowLaunch {
     const int32_t* b_cols;
     const double* b_vals;
     const int32_t* csize;
-    const int2* cpair;   // compressed B: {word index, bits} in B's own slots
+    const int2* cpair;   // compressed B: {word index, bits} in B's own slots, allocation
+                         // base; index with cpair_of(L) (rebased by b_rowptr[0])
     // rows
     const int32_t* list; // nullptr: rows [0, nrows)
     int64_t nrows;
@@ -82,8 +84,8 @@ struct RowLaunch {
 
 // kernel launchers (kk_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
-                            int32_t* csize, int2* cp, unsigned long long* nnz_bc, unsigned long long* unsorted,
-                            cudaStream_t st);
+                            int32_t* csize, int2* cp_alloc, unsigned long long* nnz_bc, unsigned long long* unsorted,
+                            const int* band, cudaStream_t st);
 cudaError_t launch_flops(int32_t m, double avg_len, const int64_t* a_rowptr,
                          const int32_t* a_cols, const int64_t* b_rowptr, const int32_t* csize,
                          int64_t* out_f, int64_t* out_cf, Totals* tot, cudaStream_t st);
@@ -186,5 +188,13 @@ cudaError_t launch_replay_numeric(ReplayLaunch R, int width, int32_t max_row, cu
 
 void count_launch(int n = 1);
 int sm_count();
+
+#ifdef __CUDACC__
+// compressed pairs indexed by absolute B positions of the (possibly offset) B view
+__device__ __forceinline__ const int2* cpair_of(const RowLaunch& L)
+{
+    return L.cpair ? L.cpair - __ldg(L.b_rowptr) : nullptr;
+}
+#endif
 
 } // namespace kk

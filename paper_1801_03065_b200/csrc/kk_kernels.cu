@@ -89,12 +89,34 @@ constexpr int32_t kShortRow = 8;
 // the running (word index, bits) pair stays in registers and is flushed when the word
 // changes; an out-of-order word (unsorted row) merges into its earlier pair.
 // Longer rows are left to the warp kernel below.
-__global__ void __launch_bounds__(256) compress_short_kernel(int32_t n, const int64_t* __restrict__ rowptr,
-                                                             const int32_t* __restrict__ cols,
-                                                             int32_t* __restrict__ csize,
-                                                             int2* __restrict__ cp, unsigned long long* nnz_bc,
-                                                             unsigned long long* unsorted)
+// The compressed pairs live in B's own slots relative to the VIEW's first
+// offset (rowptr[0] of a row-block view need not be 0): both compress kernels
+// take the unshifted allocation and rebase on the device, and work only on the
+// band [band[0], band[1]] of B rows that A references when `band` is given —
+// so the host never reads either value before launching.
+__device__ __forceinline__ void compress_band(int32_t n_all, const int* band, int32_t& j0, int32_t& n)
 {
+    j0 = 0;
+    n = n_all;
+    if (band) {
+        const int lo = __ldg(band), hi = __ldg(band + 1) + 1;
+        j0 = lo < 0 ? 0 : (lo > n_all ? n_all : lo);
+        const int e = hi < j0 ? j0 : (hi > n_all ? n_all : hi);
+        n = e - j0;
+    }
+}
+
+__global__ void __launch_bounds__(256) compress_short_kernel(int32_t n_all, const int64_t* __restrict__ rowptr_all,
+                                                             const int32_t* __restrict__ cols,
+                                                             int32_t* __restrict__ csize_all,
+                                                             int2* __restrict__ cp_alloc, unsigned long long* nnz_bc,
+                                                             unsigned long long* unsorted, const int* band)
+{
+    int32_t j0, n;
+    compress_band(n_all, band, j0, n);
+    const int64_t* __restrict__ rowptr = rowptr_all + j0;
+    int32_t* __restrict__ csize = csize_all + j0;
+    int2* __restrict__ cp = cp_alloc - __ldg(rowptr_all);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned long long pairs = 0;
     bool sorted = true;
@@ -185,12 +207,17 @@ __device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32
 // of 32 consecutive rows: one coalesced load of their offsets, then the long
 // rows of the batch (ballot) one after another, the next row's columns
 // loaded while the current one is compressed.
-__global__ void __launch_bounds__(256) compress_kernel(int32_t n, const int64_t* __restrict__ rowptr,
+__global__ void __launch_bounds__(256) compress_kernel(int32_t n_all, const int64_t* __restrict__ rowptr_all,
                                                        const int32_t* __restrict__ cols,
-                                                       int32_t* __restrict__ csize,
-                                                       int2* __restrict__ cp, unsigned long long* nnz_bc,
-                                                       unsigned long long* unsorted)
+                                                       int32_t* __restrict__ csize_all,
+                                                       int2* __restrict__ cp_alloc, unsigned long long* nnz_bc,
+                                                       unsigned long long* unsorted, const int* band)
 {
+    int32_t j0, n;
+    compress_band(n_all, band, j0, n);
+    const int64_t* __restrict__ rowptr = rowptr_all + j0;
+    int32_t* __restrict__ csize = csize_all + j0;
+    int2* __restrict__ cp = cp_alloc - __ldg(rowptr_all);
     const int lane = threadIdx.x & 31;
     unsigned long long pairs = 0; // warp-uniform
     bool sorted = true;           // warp-uniform
@@ -339,7 +366,7 @@ __global__ void __launch_bounds__(256, 8) flops_kernel(int32_t m, const int64_t*
     __syncthreads();
     const int glane = threadIdx.x & (G - 1);
     const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
-    unsigned long long my_tf = 0, my_mf = 0, my_tcf = 0, my_mcf = 0;
+    unsigned long long my_tf = 0, my_mf = 0, my_tcf = 0, my_mcf = 0, my_ma = 0;
     const int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
     // uniform trip count per warp so the group shuffles stay converged; two
     // rows per group per trip, their loads issued together (the chain
@@ -390,6 +417,7 @@ __global__ void __launch_bounds__(256, 8) flops_kernel(int32_t m, const int64_t*
             }
             const bool owner = glane == 0 && i < m;
             if (owner) {
+                my_ma = max(my_ma, (unsigned long long)(end[u] - beg[u]));
                 out_f[i] = f;
                 out_cf[i] = cf;
                 my_tf += f;
@@ -407,12 +435,14 @@ __global__ void __launch_bounds__(256, 8) flops_kernel(int32_t m, const int64_t*
         my_tcf += __shfl_xor_sync(kFull, my_tcf, off);
         my_mf = max(my_mf, __shfl_xor_sync(kFull, my_mf, off));
         my_mcf = max(my_mcf, __shfl_xor_sync(kFull, my_mcf, off));
+        my_ma = max(my_ma, __shfl_xor_sync(kFull, my_ma, off));
     }
     if ((threadIdx.x & 31) == 0) {
         atomicAdd(&tot->total_f, my_tf);
         atomicAdd(&tot->total_cf, my_tcf);
         atomicMax(&tot->max_f, my_mf);
         atomicMax(&tot->max_cf, my_mcf);
+        atomicMax(&tot->max_alen, my_ma);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < 128; t += blockDim.x) {
@@ -598,7 +628,7 @@ __global__ void __launch_bounds__(256) row_kernel(const RowLaunch L)
             cnt = warp_row<kFlat, true>(L.a_rowptr, L.a_cols, nullptr, i, src, map, ids, pay,
                                         cap, L.ctr, lane, L.l1_keys, spill);
         } else {
-            const CompressedSource src{L.b_rowptr, L.csize, L.cpair};
+            const CompressedSource src{L.b_rowptr, L.csize, cpair_of(L)};
             cnt = warp_row<kFlat, false>(L.a_rowptr, L.a_cols, nullptr, i, src, map, ids, pay,
                                          cap, L.ctr, lane, L.l1_keys, spill);
         }
@@ -1191,18 +1221,18 @@ cudaError_t launch_sort_rows(int32_t m, const int64_t* rowptr, int32_t* cols, do
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_compress(int32_t n, const int64_t* b_rowptr, const int32_t* b_cols,
-                            int32_t* csize, int2* cp, unsigned long long* nnz_bc, unsigned long long* unsorted,
-                            cudaStream_t st)
+                            int32_t* csize, int2* cp_alloc, unsigned long long* nnz_bc, unsigned long long* unsorted,
+                            const int* band, cudaStream_t st)
 {
     if (n <= 0)
         return cudaSuccess;
     // short rows: thread per row; longer rows: warp per row in batches of 32
     const int tblocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
-    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp, nnz_bc, unsorted);
+    compress_short_kernel<<<tblocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp_alloc, nnz_bc, unsorted, band);
     count_launch();
     const int64_t batches = (n + 31) / 32;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((batches + 7) / 8, (int64_t)sm_count() * 8));
-    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp, nnz_bc, unsorted);
+    compress_kernel<<<blocks, 256, 0, st>>>(n, b_rowptr, b_cols, csize, cp_alloc, nnz_bc, unsorted, band);
     count_launch();
     return cudaGetLastError();
 }
