@@ -139,7 +139,7 @@ __device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ c
 // Optional phase profile (-DKK_SLAB_PROF): lane 0 of every warp adds clock
 // deltas and event counts; read with spg_debug_slab_prof.
 #ifdef KK_SLAB_PROF
-__device__ unsigned long long g_slab_prof[16];
+__device__ unsigned long long g_slab_prof[64];
 #define PROF_DECL unsigned long long prof_t = clock64();
 #define PROF_MARK(idx)                                                                                   \
     do {                                                                                                 \
@@ -304,6 +304,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const Row
             continue;
         }
         const int64_t C_lo = S.k * part / parts, C_hi = S.k * (part + 1) / parts;
+#ifdef KK_SLAB_PROF
+        const unsigned long long item_t0 = clock64();
+        const int dcls = d <= 1 ? 0 : min(15, 64 - __clzll(static_cast<unsigned long long>(d - 1)));
+#endif
         // ---- cursors at the part's first column ----
         for (int64_t p0 = 0; p0 < d; p0 += 32) {
             const int64_t p = p0 + lane;
@@ -576,6 +580,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const Row
                 raise_error(L.ctr, kDevUnsorted);
             continue;
         }
+#ifdef KK_SLAB_PROF
+        if (lane == 0) {
+            atomicAdd(&g_slab_prof[16 + dcls], clock64() - item_t0);
+            atomicAdd(&g_slab_prof[32 + dcls], static_cast<unsigned long long>(emitted));
+            atomicAdd(&g_slab_prof[48 + dcls], 1ull);
+        }
+#endif
         if (lane == 0) {
             if (parts == 1) {
                 if (emitted != cap)
@@ -633,7 +644,7 @@ extern "C" int spg_debug_slab_prof(unsigned long long* out, int reset)
     if (out)
         cudaMemcpyFromSymbol(out, kk::g_slab_prof, sizeof(kk::g_slab_prof));
     if (reset) {
-        unsigned long long z[16] = {};
+        unsigned long long z[64] = {};
         cudaMemcpyToSymbol(kk::g_slab_prof, z, sizeof(z));
     }
     return 1;

@@ -17,7 +17,7 @@ h = kk.symbolic(A, A)
 L = kk.lib()
 f = L.spg_debug_slab_prof
 f.argtypes = [C.c_void_p, C.c_int]
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 64)()
 c = kk.numeric(A, A, h)
 torch.cuda.synchronize()
 f(None, 1)
@@ -33,3 +33,8 @@ print(f"s{scale} numeric {e0.elapsed_time(e1):.2f} ms heavy_path={h.heavy_path}"
 for n, v in zip(names, buf):
     if n:
         print(f"  {n:16s} {v:>18,d}")
+print("  by A-row length class (item cycles, outputs, items):")
+tot = sum(buf[16:32]) or 1
+for c in range(16):
+    if buf[48 + c]:
+        print(f"   d<=2^{c:2d}: {100 * buf[16 + c] / tot:5.1f}% cycles  outputs {buf[32 + c]:>14,d}  items {buf[48 + c]:>8,d}")
