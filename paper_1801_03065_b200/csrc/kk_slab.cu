@@ -337,13 +337,21 @@ __global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const Row
             //      32 entries per step (independent loads in flight) ----
             int64_t prods = 0;
             int32_t nr = 0;
+            // the next step's cursors are loaded while this step probes B
+            Cursor fa{0, 0, INT_MAX}, fb{0, 0, INT_MAX};
+            if (lane < d)
+                fa = ws.cur[lane];
+            if (32 + lane < d)
+                fb = ws.cur[32 + lane];
             for (int64_t p0 = 0; p0 < d; p0 += 64) {
                 const int64_t pa = p0 + lane, pb = p0 + 32 + lane;
-                Cursor ca{0, 0, INT_MAX}, cb{0, 0, INT_MAX};
-                if (pa < d)
-                    ca = ws.cur[pa];
-                if (pb < d)
-                    cb = ws.cur[pb];
+                const Cursor ca = fa, cb = fb;
+                fa = Cursor{0, 0, INT_MAX};
+                fb = Cursor{0, 0, INT_MAX};
+                if (pa + 64 < d)
+                    fa = ws.cur[pa + 64];
+                if (pb + 64 < d)
+                    fb = ws.cur[pb + 64];
                 const bool na = ca.nxt < c_hi, nb = cb.nxt < c_hi;
                 bad = bad || (na && ca.nxt < c_lo) || (nb && cb.nxt < c_lo); // an earlier run ended early: unsorted B row
                 int32_t xa = INT_MAX, xb = INT_MAX;
