@@ -46,10 +46,16 @@ namespace kk {
 
 namespace {
 
-constexpr int kWarps = 8;           // independent warps per CTA
-constexpr int kTW = 1024;           // table slots per warp
-constexpr int kTWMax = 768;         // keys before a slab is abandoned
-constexpr int kX = 600;             // target distinct keys per slab
+#ifndef KK_SLAB_LOG2_TW
+#define KK_SLAB_LOG2_TW 9 // table slots per warp (A/B builds: -DKK_SLAB_LOG2_TW=9 -DKK_SLAB_CTAS=3)
+#endif
+#ifndef KK_SLAB_CTAS
+#define KK_SLAB_CTAS 3 // resident CTAs per SM the kernel is compiled for
+#endif
+constexpr int kWarps = 8;                          // independent warps per CTA
+constexpr int kTW = 1 << KK_SLAB_LOG2_TW;          // table slots per warp
+constexpr int kTWMax = kTW * 3 / 4;                // keys before a slab is abandoned
+constexpr int kX = kTW * 600 / 1024;               // target distinct keys per slab
 constexpr double kSplitWork = 4e8;  // A-row length x row size per part
 
 
@@ -59,7 +65,7 @@ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ?
 
 __device__ __forceinline__ uint32_t key_slot(int32_t key)
 {
-    return (static_cast<uint32_t>(key) * 0x9E3779B1u) >> 22; // 10 bits
+    return (static_cast<uint32_t>(key) * 0x9E3779B1u) >> (32 - KK_SLAB_LOG2_TW);
 }
 
 // Run-end search, split so that two A entries' first loads are in flight
@@ -270,7 +276,7 @@ __device__ __forceinline__ void fold(bool valid, int32_t key, double v, WarpSmem
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 2) numeric_wslab_kernel(const RowLaunch L, const SlabArgs S)
+__global__ void __launch_bounds__(kWarps * 32, KK_SLAB_CTAS) numeric_wslab_kernel(const RowLaunch L, const SlabArgs S)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
