@@ -453,9 +453,33 @@ def run_gpu(args, rank, world, local):
             line[k] = res[k]
     line.update(extra)
     print(json.dumps(line), flush=True)
+    if args.csv:
+        write_records(args.csv, line, res)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def write_records(path, line, res):
+    """The line as the reference's BenchRecord rows (bench.cpp:28-102; the
+    reference CLI's `bench` output, cli.cpp:132-174): one NoReuse row and one
+    reuse (numeric-only) row, GPU columns in the sidecar .gpu.csv."""
+    import torch
+    from paper_1801_03065_b200 import harness as H
+    cfg = line["config"]
+    det = res.get("detail") or {}
+    base = dict(problem=cfg["workload"].split(":")[0], scheme="gpu", m=cfg["m"], n=cfg["m"], k=cfg["m"],
+                nnz_a=cfg["nnz_a"], nnz_b=cfg["nnz_a"], flops=cfg["flops"], nnz_c=cfg["nnz_c"],
+                max_row_size=int(det.get("max_row_size", 0)), threads=1, device=torch.cuda.get_device_name(),
+                n_gpus=line["n_gpus"])
+    rs = [H.BenchRecord(algorithm="kk-b200", reps=line["steps"], t_total_ms=line["ms_per_step"],
+                        gflops=line["value"], roofline_frac=line["roofline"]["frac"], **base)]
+    no = line.get("numeric_only") or {}
+    if no.get("ms_per_step"):
+        rs.append(H.BenchRecord(algorithm="kk-b200-reuse", reps=line["steps"], reuse=True,
+                                t_numeric_ms=no["ms_per_step"], t_total_ms=no["ms_per_step"],
+                                gflops=no.get("value") or 0.0, **base))
+    H.write_bench_csv(path, rs)
 
 
 def _sym_bytes(info, m, n_b):
@@ -875,6 +899,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--csv", default=None, help="also write the line as a BenchRecord CSV (bench.cpp:28-102)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3 if args.impl == "kk" else args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

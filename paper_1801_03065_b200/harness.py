@@ -154,7 +154,7 @@ def bench_problem(problem: str, a, b, cfg=None, reps: int = 5, reuse: int = 0, l
     events), optional reuse record of numeric-only passes."""
     import torch
     import paper_1801_03065_b200 as kk
-    from bench import algorithmic_bytes_numeric, _peaks
+    from bench import bytes_num as algorithmic_bytes_numeric, _peaks
     da, db = kk._dev(a), kk._dev(b)
     warm = kk.multiply(da, db, cfg)
     h = warm.handle
@@ -214,8 +214,8 @@ def main(argv=None) -> int:
         return 0
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
-    from bench import workload
-    a, wl = workload(args.config, args.scale)
+    from bench import operand_a
+    a, wl = operand_a(args.config, args.scale)
     recs = bench_problem(f"c{args.config}", a, a, reps=args.reps, reuse=args.reuse)
     write_bench_csv(args.out, recs)
     print(f"wrote {len(recs)} record(s) for {wl} to {args.out}")

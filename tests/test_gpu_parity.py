@@ -1115,3 +1115,17 @@ def test_c4_rmat_s20_all_rows(kk, oracle):
     tc, tv = oracle.sort_rows(sro, gc, gv)
     assert np.array_equal(sc, tc)
     assert np.array_equal(sv.view(np.int64), tv.view(np.int64))
+
+
+def test_harness_bench_rows_on_gpu(tmp_path):
+    """harness bench (cli.cpp:132-174 on the GPU) writes the reference's
+    22-column BenchRecord rows; the profile reads them back."""
+    from paper_1801_03065_b200 import harness as H
+    out = tmp_path / "r.csv"
+    assert H.main(["bench", "--config", "2", "--scale", "0.1", "--reps", "2", "--reuse", "2", "--out", str(out)]) == 0
+    recs = H.read_bench_csv(str(out))
+    assert [r.algorithm for r in recs] == ["auto", "auto-reuse"] and recs[1].reuse
+    assert recs[0].flops == (9 * 16 - 10) ** 3 and recs[0].nnz_c == (5 * 16 - 6) ** 3 and recs[0].gflops > 0 and recs[1].gflops > 0
+    assert open(str(out)).read().splitlines()[0] == H.HEADER
+    prof = tmp_path / "p.csv"
+    assert H.main(["profile", "--in", str(out), "--out", str(prof), "--points", "4"]) == 0
