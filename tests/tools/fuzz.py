@@ -52,6 +52,21 @@ def skewed_csr(rng, m, n, density, shuffle):
     return kk.CsrMatrix(m, n, ro, ci, v, not shuffle)
 
 
+def wide_csr(rng, m, n, density, shuffle):
+    """Random CSR over many columns (sampling with replacement, duplicates
+    dropped) — random_csr's per-row permutation is too slow at n ~ 1e5."""
+    cnt = rng.binomial(n, density, m) if n > 0 else np.zeros(m, np.int64)
+    key = np.sort(np.repeat(np.arange(m, dtype=np.int64), cnt) * max(n, 1)
+                  + rng.integers(0, max(n, 1), int(cnt.sum())))
+    key = key[np.concatenate(([True], key[1:] != key[:-1]))] if len(key) else key
+    rows, ci = key // max(n, 1), (key % max(n, 1)).astype(np.int32)
+    ro = np.zeros(m + 1, np.int64)
+    ro[1:] = np.cumsum(np.bincount(rows, minlength=m))
+    if shuffle:
+        ci = ci[np.argsort(rows + rng.random(len(ci)))]
+    return kk.CsrMatrix(m, n, ro, ci, rng.uniform(-1, 1, len(ci)), not shuffle)
+
+
 def check(o, a, b, c, raw):
     ro = o.symbolic_row_offsets(a, b)
     assert np.array_equal(c.row_offsets, ro), "row offsets"
@@ -65,7 +80,13 @@ def check(o, a, b, c, raw):
 
 
 def one_case(rng, o):
-    if rng.random() < 0.1:
+    u = rng.random()
+    if u < 0.06:
+        # long A rows over wide B: many column slabs per row, replans and
+        # table-overflow aborts in the column-slab kernel
+        m, n, k = int(rng.integers(1, 12)), int(rng.integers(1000, 4000)), int(rng.integers(20000, 200000))
+        da, db = float(rng.choice([0.1, 0.3, 0.6])), float(rng.choice([0.002, 0.005, 0.01]))
+    elif u < 0.16:
         # a few rows beyond the warp tables (heavy CTA path / L2 pool)
         m, n, k = int(rng.integers(1, 48)), int(rng.integers(500, 3000)), int(rng.integers(3000, 30000))
         da, db = float(rng.choice([0.02, 0.08])), float(rng.choice([0.01, 0.03]))
@@ -74,8 +95,12 @@ def one_case(rng, o):
         da = float(rng.choice([0.005, 0.02, 0.08, 0.2]))
         db = float(rng.choice([0.005, 0.02, 0.08, 0.2]))
     shuffle = bool(rng.random() < 0.3)
-    a = skewed_csr(rng, m, n, da, shuffle)
-    b = skewed_csr(rng, n, k, db, shuffle)
+    if u < 0.06:
+        a = wide_csr(rng, m, n, da, shuffle)
+        b = wide_csr(rng, n, k, db, shuffle)
+    else:
+        a = skewed_csr(rng, m, n, da, shuffle)
+        b = skewed_csr(rng, n, k, db, shuffle)
     acc = int(rng.choice([0, 0, 0, 1, 2, 3]))
     cfg = kk.SpgemmConfig(accumulator=acc, scheme=int(rng.integers(0, 2)),
                           l1_capacity=int(rng.choice([0, 0, 0, 1, 16])) if acc != 3 else 0,
