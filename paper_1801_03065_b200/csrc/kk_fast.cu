@@ -597,7 +597,6 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
     const int T = L.lay.T;
     const uint32_t tmask = static_cast<uint32_t>(T - 1);
     const int pshift = L.lay.shift;
-    const int32_t cap = L.lay.S;
     for (int t = lane; t < T; t += 32) {
         keys[t] = kEmpty;
         words[t] = 0u;
@@ -606,45 +605,34 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
 
     const int64_t nwarps = (int64_t)gridDim.x * L.wpb;
     const int64_t* __restrict__ b_rowptr = L.b_rowptr;
-    int32_t used = 0; // claimed slots of the current row (warp-uniform)
-    bool overflow = false;
-    bool prev_claimed = false;
+    bool overflow = false; // the current row's table filled up
 
     // one chunk of <= 32 A entries of the current row, B-row descriptors in registers
     auto chunk = [&](int na, int64_t bb, int32_t bl) {
-            // probe / claim / OR one (key, word); true when this lane claimed a slot
+            // probe / claim / OR one (key, word); false only when the table is
+            // full (the row is then handed to the exact-size path).  Rows past
+            // the optimistic key count but within the table complete here.
             auto insert = [&](int32_t key, uint32_t word) -> bool {
-                bool claimed = false;
-                if (key != kEmpty) {
-                    uint32_t s = loc_hash(key, pshift);
-                    for (int probes = 0; probes <= T; ++probes) {
-                        const int32_t k = keys[s];
-                        if (k == key)
-                            break;
-                        if (k == kEmpty) {
-                            const int32_t old = atomicCAS(&keys[s], kEmpty, key);
-                            if (old == kEmpty) {
-                                claimed = true;
-                                break;
-                            }
-                            if (old == key)
-                                break;
-                        }
-                        s = (s + kProbeStep) & tmask;
+                if (key == kEmpty)
+                    return true;
+                uint32_t s = loc_hash(key, pshift);
+                for (int probes = 0; probes < T; ++probes) {
+                    const int32_t k = keys[s];
+                    bool hit = k == key;
+                    if (k == kEmpty) {
+                        const int32_t old = atomicCAS(&keys[s], kEmpty, key);
+                        hit = old == kEmpty || old == key;
                     }
-                    if constexpr (kCompressed)
-                        atomicOr(&words[s], word);
+                    if (hit) {
+                        if constexpr (kCompressed)
+                            atomicOr(&words[s], word);
+                        return true;
+                    }
+                    s = (s + kProbeStep) & tmask;
                 }
-                return claimed;
+                return false;
             };
-            // claims are counted one step late (the ballot then never waits on
-            // this step's CAS); a table can fill up before the count sees it,
-            // but such a row is always flagged at its end
-            auto account = [&](bool claimed) {
-                used += __popc(__ballot_sync(kFull, prev_claimed));
-                prev_claimed = claimed;
-                return used > cap; // table too small for this row: hand it to the L2 path
-            };
+            auto full = [&](bool ok) { return __any_sync(kFull, !ok); };
             auto load = [&](int64_t q, int32_t& key, uint32_t& word) {
                 if constexpr (kCompressed) {
                     const int2 pr = __ldg(cpair + q);
@@ -659,7 +647,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
             const int lg = maxbl <= 1 ? 0 : 32 - __clz(maxbl - 1);
             const int G = 32 >> lg;
             const int32_t csum = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<unsigned>(bl)));
-            if (!L.no_segments && maxbl <= 16 && (na + G - 1) / G <= (csum + 31) / 32) {
+            if (!L.no_segments && maxbl <= 16 && ((na + G - 1) >> (5 - lg)) <= ((csum + 31) >> 5)) {
                 // short (compressed) B rows: segmented steps — G = 32/Lw B rows
                 // per step, Lw = pow2 >= the longest, lane = (row, entry); the
                 // union is order-free, so no flattened-index mapping is needed.
@@ -684,7 +672,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                     const uint32_t word = nword;
                     if (q0 + G < na)
                         sfetch(q0 + G, nkey, nword);
-                    if (account(insert(key, word))) {
+                    if (full(insert(key, word))) {
                         overflow = true;
                         break;
                     }
@@ -714,7 +702,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                 const uint32_t word = nword;
                 if (w0 + 32 < total)
                     fetch(w0 + 32, nkey, nword);
-                if (account(insert(key, word))) {
+                if (full(insert(key, word))) {
                     overflow = true;
                     break;
                 }
@@ -722,8 +710,6 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
     };
     // size of the finished row (or its hand-off to the L2 path); table reset
     auto finish = [&](int32_t i) {
-        used += __popc(__ballot_sync(kFull, prev_claimed));
-        overflow = overflow || used > cap;
         __syncwarp();
         int64_t size = 0;
         for (int t = lane; t < T; t += 32) {
@@ -743,9 +729,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                 L.sym_sizes[i] = size;
         }
         __syncwarp();
-        used = 0;
         overflow = false;
-        prev_claimed = false;
     };
 
     if constexpr (!kPipe) {

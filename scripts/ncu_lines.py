@@ -1,30 +1,28 @@
-"""Summarise an ncu source page (cuda,sass view): top source lines by stall samples,
-with executed instructions and shared-memory / global wavefront columns."""
-import csv, subprocess, sys
-rep, skip = sys.argv[1], sys.argv[2]
-n = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass",
-                      "--launch-skip", skip, "--launch-count", "1"], capture_output=True, text=True).stdout
-rows = list(csv.reader(out.splitlines()))
-hdr = None; cur = None; res = []
-for r in rows:
-    if len(r) >= 2 and r[0] == "File Path":
-        cur = r[1].split("/")[-1]; continue
-    if r and r[0] == "Line No":
-        hdr = r; continue
-    if hdr is None or len(r) < 8:
-        continue
-    def col(name):
+"""Per-CUDA-source-line stall samples and executed instructions of an ncu
+report (captured with --import-source on).  Usage: python scripts/ncu_lines.py rep [N]"""
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+raw = subprocess.run(["ncu", "-i", rep, *sys.argv[3:], "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+cur, hdr, out = None, None, []
+for r in csv.reader(raw.splitlines()):
+    if len(r) == 2 and r[0] == "File Path":
+        cur = r[1].split("/")[-1]
+    elif r and r[0] == "Line No":
+        hdr = r
+    elif hdr and r and r[0] and len(r) == len(hdr):
         try:
-            return int(float(r[hdr.index(name)] or 0))
-        except (ValueError, IndexError):
-            return 0
-    if r[0] != "":
-        res.append((col("Warp Stall Sampling (All Samples)"), col("Instructions Executed"),
-                    col("L1 Wavefronts Shared"), col("L1 Wavefronts Shared Ideal"),
-                    col("L2 Theoretical Sectors Global"), f"{cur}:{r[0]}", r[1][:80]))
-ts = sum(x[0] for x in res); ti = sum(x[1] for x in res); tw = sum(x[2] for x in res)
-print(f"samples {ts} warp-instructions {ti} smem-wavefronts {tw}")
-print("samples   %   instrs     smem_wf  smem_ideal  l2_sect  line")
-for o in sorted(res, reverse=True)[:n]:
-    print(f"{o[0]:7d} {o[0]/max(ts,1)*100:5.1f} {o[1]:11d} {o[2]:11d} {o[3]:11d} {o[4]:10d} {o[5]} {o[6]}")
+            out.append((cur, int(r[0]), r[1][:72], float(r[4] or 0), float(r[7] or 0)))
+        except ValueError:
+            pass
+ts = sum(o[3] for o in out) or 1
+te = sum(o[4] for o in out) or 1
+print(f"samples {ts:.0f}, warp instructions {te:.3e}")
+for key, label in ((3, "by stall samples"), (4, "by executed instructions")):
+    print(f"-- {label}")
+    for o in sorted(out, key=lambda o: -o[key])[:n]:
+        print(f"{o[0]:16s}{o[1]:5d} {100 * o[3] / ts:5.1f}% smp {100 * o[4] / te:5.1f}% ins  {o[2]}")
