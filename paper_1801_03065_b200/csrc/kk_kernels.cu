@@ -74,6 +74,22 @@ __device__ __forceinline__ uint32_t group_or(uint32_t grp, uint32_t v, int lane)
     return acc;
 }
 
+// group_or through a per-warp 32-word shared buffer (zero on entry and on
+// return): members OR into their leader's word, then read it back.
+__device__ __forceinline__ uint32_t group_or_smem(uint32_t grp, uint32_t v, int lane, uint32_t* buf)
+{
+    const int leader = __ffs(grp) - 1;
+    if (v)
+        atomicOr(&buf[leader], v);
+    __syncwarp();
+    const uint32_t r = buf[leader];
+    __syncwarp();
+    if (lane == leader)
+        buf[lane] = 0u;
+    __syncwarp();
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // K3: graph compression of B, written into B's own slots (pairs of row j at
 // [rowptr[j], rowptr[j] + csize[j])).  Warp per row.  Pair order is the
@@ -83,7 +99,10 @@ __device__ __forceinline__ uint32_t group_or(uint32_t grp, uint32_t v, int lane)
 // ---------------------------------------------------------------------------
 // rows up to this length are compressed by one thread (aggregation/AP rows);
 // longer ones (stencils: 27) by a warp, whose loads coalesce
-constexpr int32_t kShortRow = 8;
+#ifndef KK_SHORT_ROW
+#define KK_SHORT_ROW 8
+#endif
+constexpr int32_t kShortRow = KK_SHORT_ROW;
 
 // Thread per B row for rows of <= kShortRow entries:
 // the running (word index, bits) pair stays in registers and is flushed when the word
@@ -104,6 +123,52 @@ __device__ __forceinline__ void compress_band(int32_t n_all, const int* band, in
         const int e = hi < j0 ? j0 : (hi > n_all ? n_all : hi);
         n = e - j0;
     }
+}
+
+// One thread compresses one row, entry by entry (rc: the row's columns, in
+// global or shared memory): a run of one word extends the open pair; a word
+// at or below the largest seen so far may merge into an earlier pair (rows
+// that are not column-sorted), first-touch order kept.  Returns the pair count.
+__device__ __forceinline__ int32_t compress_row_seq(const int32_t* __restrict__ rc, int32_t len, int64_t lo,
+                                                    int2* __restrict__ cp,
+                                                    bool& sorted)
+{
+    int32_t np = 0, cur_w = -1, maxw = -1, prev_c = INT_MIN;
+    uint32_t cur = 0;
+    for (int32_t q = 0; q < len; ++q) {
+        const int32_t c = rc[q];
+        sorted = sorted && c > prev_c;
+        prev_c = c;
+        const int32_t w = c >> 5;
+        const uint32_t bit = 1u << (c & 31);
+        if (w == cur_w) {
+            cur |= bit;
+            continue;
+        }
+        int32_t found = -1;
+        if (w <= maxw) // not beyond every word seen so far: maybe an earlier pair
+            for (int32_t t = 0; t < np; ++t)
+                if (cp[lo + t].x == w) {
+                    found = t;
+                    break;
+                }
+        if (cur_w >= 0) { // flush the running pair
+            cp[lo + np - 1].y = static_cast<int>(cur);
+            cur_w = -1;
+        }
+        if (found >= 0) { // merge into the earlier pair, in place (first-touch order kept)
+            cp[lo + found].y |= static_cast<int>(bit);
+            continue;
+        }
+        cp[lo + np].x = w;
+        ++np;
+        cur_w = w;
+        cur = bit;
+        maxw = max(maxw, w);
+    }
+    if (cur_w >= 0)
+        cp[lo + np - 1].y = static_cast<int>(cur);
+    return np;
 }
 
 __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n_all, const int64_t* __restrict__ rowptr_all,
@@ -132,41 +197,7 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n_all, cons
         const bool is_long = j < n && len > kShortRow;
         if (j >= n || is_long)
             continue;
-        int32_t np = 0, cur_w = -1, maxw = -1, prev_c = INT_MIN;
-        uint32_t cur = 0;
-        for (int32_t q = 0; q < len; ++q) {
-            const int32_t c = __ldg(cols + lo + q);
-            sorted = sorted && c > prev_c;
-            prev_c = c;
-            const int32_t w = c >> 5;
-            const uint32_t bit = 1u << (c & 31);
-            if (w == cur_w) {
-                cur |= bit;
-                continue;
-            }
-            int32_t found = -1;
-            if (w <= maxw) // not beyond every word seen so far: maybe an earlier pair
-                for (int32_t t = 0; t < np; ++t)
-                    if (cp[lo + t].x == w) {
-                        found = t;
-                        break;
-                    }
-            if (cur_w >= 0) { // flush the running pair
-                cp[lo + np - 1].y = static_cast<int>(cur);
-                cur_w = -1;
-            }
-            if (found >= 0) { // merge into the earlier pair, in place (first-touch order kept)
-                cp[lo + found].y |= static_cast<int>(bit);
-                continue;
-            }
-            cp[lo + np].x = w;
-            ++np;
-            cur_w = w;
-            cur = bit;
-            maxw = max(maxw, w);
-        }
-        if (cur_w >= 0)
-            cp[lo + np - 1].y = static_cast<int>(cur);
+        const int32_t np = compress_row_seq(cols + lo, len, lo, cp, sorted);
         csize[j] = np;
         pairs += static_cast<unsigned long long>(np);
     }
@@ -181,13 +212,13 @@ __global__ void __launch_bounds__(256) compress_short_kernel(int32_t n_all, cons
 
 __device__ __forceinline__ int compress_row_short(int64_t j, int64_t lo, int64_t len, int32_t col, int lane,
                                                   int32_t* __restrict__ csize, int2* __restrict__ cp,
-                                                  bool* sorted_out)
+                                                  bool* sorted_out, uint32_t* orbuf)
 {
     const bool valid = lane < len;
     const int32_t w = col >> 5;
     const int32_t key = valid ? w : -1 - lane;
     const uint32_t grp = __match_any_sync(kFull, key);
-    const uint32_t orv = group_or(grp, valid ? (1u << (col & 31)) : 0u, lane);
+    const uint32_t orv = group_or_smem(grp, valid ? (1u << (col & 31)) : 0u, lane, orbuf);
     const bool leader = valid && (__ffs(grp) - 1) == lane;
     const uint32_t lm = __ballot_sync(kFull, leader);
     const int32_t prev = __shfl_up_sync(kFull, col, 1);
@@ -204,9 +235,12 @@ __device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32
                                  int32_t* __restrict__ csize, int2* __restrict__ cp, bool* sorted_out);
 
 // Warp kernel for rows of more than kShortRow entries.  A warp takes batches
-// of 32 consecutive rows: one coalesced load of their offsets, then the long
-// rows of the batch (ballot) one after another, the next row's columns
-// loaded while the current one is compressed.
+// of 32 consecutive rows: one coalesced load of their offsets; when the
+// batch's entries fit the warp's stage (kCompressStage columns) they are
+// copied in with all loads in flight, and each row is compressed from shared
+// memory; otherwise the long rows of the batch (ballot) go one after another,
+// the next row's columns loaded while the current one is compressed.
+constexpr int kCompressStage = 1024;
 __global__ void __launch_bounds__(256) compress_kernel(int32_t n_all, const int64_t* __restrict__ rowptr_all,
                                                        const int32_t* __restrict__ cols,
                                                        int32_t* __restrict__ csize_all,
@@ -219,6 +253,12 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n_all, const int6
     int32_t* __restrict__ csize = csize_all + j0;
     int2* __restrict__ cp = cp_alloc - __ldg(rowptr_all);
     const int lane = threadIdx.x & 31;
+    __shared__ int32_t stage_all[8][kCompressStage];
+    __shared__ uint32_t orbuf_all[8][32];
+    int32_t* stage = stage_all[threadIdx.x >> 5];
+    uint32_t* orbuf = orbuf_all[threadIdx.x >> 5];
+    orbuf[lane] = 0u;
+    __syncwarp();
     unsigned long long pairs = 0; // warp-uniform
     bool sorted = true;           // warp-uniform
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -230,6 +270,28 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n_all, const int6
             blen = __ldg(rowptr + jr + 1) - blo;
         }
         uint32_t todo = __ballot_sync(kFull, jr < n && blen > kShortRow);
+        if (!todo)
+            continue;
+        const int nb = n - r0 < 32 ? static_cast<int>(n - r0) : 32;
+        const int64_t sbase = __shfl_sync(kFull, blo, 0);
+        const int64_t stot = __shfl_sync(kFull, blo + blen, nb - 1) - sbase;
+        if (stot <= kCompressStage && __all_sync(kFull, blen <= 32)) {
+            // staged batch: every column load in flight at once
+#pragma unroll 4
+            for (int t = lane; t < stot; t += 32)
+                stage[t] = __ldg(cols + sbase + t);
+            __syncwarp();
+            while (todo) {
+                const int q = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int64_t lo = __shfl_sync(kFull, blo, q);
+                const int64_t len = __shfl_sync(kFull, blen, q);
+                const int32_t col = lane < len ? stage[lo - sbase + lane] : 0;
+                pairs += compress_row_short(r0 + q, lo, len, col, lane, csize, cp, &sorted, orbuf);
+            }
+            __syncwarp();
+            continue;
+        }
         auto pop = [&]() {
             const int q = todo ? __ffs(todo) - 1 : -1;
             todo &= todo - 1;
@@ -244,7 +306,7 @@ __global__ void __launch_bounds__(256) compress_kernel(int32_t n_all, const int6
         };
         auto process = [&](int q, int64_t lo, int64_t len, int32_t col) {
             if (len <= 32)
-                pairs += compress_row_short(r0 + q, lo, len, col, lane, csize, cp, &sorted);
+                pairs += compress_row_short(r0 + q, lo, len, col, lane, csize, cp, &sorted, orbuf);
             else
                 pairs += compress_row_long(r0 + q, lo, len, cols, lane, csize, cp, &sorted);
         };
@@ -353,7 +415,10 @@ __device__ int compress_row_long(int64_t j, int64_t lo, int64_t len, const int32
 // without another pass).  G lanes per A row.
 // ---------------------------------------------------------------------------
 template <int G>
-__global__ void __launch_bounds__(256, 8) flops_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,
+#ifndef KK_FLOPS_MINB
+#define KK_FLOPS_MINB 4 // 64 registers: no spills (c2 0.71 -> 0.57 ms vs 8)
+#endif
+__global__ void __launch_bounds__(256, KK_FLOPS_MINB) flops_kernel(int32_t m, const int64_t* __restrict__ a_rowptr,
                                                     const int32_t* __restrict__ a_cols,
                                                     const int64_t* __restrict__ b_rowptr,
                                                     const int32_t* __restrict__ csize,
