@@ -55,8 +55,18 @@ namespace {
 constexpr int kWarps = 8;                          // independent warps per CTA
 constexpr int kTW = 1 << KK_SLAB_LOG2_TW;          // table slots per warp
 constexpr int kTWMax = kTW * 3 / 4;                // keys before a slab is abandoned
-constexpr int kX = kTW * 600 / 1024;               // target distinct keys per slab
+#ifndef KK_SLAB_XFRAC
+#define KK_SLAB_XFRAC 500 // target keys per slab, per 1024 table slots
+#endif
+#ifndef KK_SLAB_ACCEPT
+#define KK_SLAB_ACCEPT 1.45 // a planned slab predicted above ACCEPT * kX keys is re-planned narrower
+#endif
+constexpr int kX = kTW * KK_SLAB_XFRAC / 1024;     // target distinct keys per slab
 constexpr double kSplitWork = 4e8;  // A-row length x row size per part
+#ifndef KK_SLAB_DEPTH
+#define KK_SLAB_DEPTH 2 // mapped windows in flight ahead of the one being folded
+#endif
+constexpr int kDepth = KK_SLAB_DEPTH;
 
 
 
@@ -399,6 +409,8 @@ __global__ void __launch_bounds__(kWarps * 32, KK_SLAB_CTAS) numeric_wslab_kerne
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1)
                 prods += __shfl_xor_sync(kFull, prods, o);
+            PROF_COUNT(14, nr);
+            PROF_COUNT(15, d);
             if (__any_sync(kFull, bad)) {
                 bad = true;
                 break;
@@ -411,12 +423,14 @@ __global__ void __launch_bounds__(kWarps * 32, KK_SLAB_CTAS) numeric_wslab_kerne
                 const double est = static_cast<double>(prods) * ratio;
                 const int64_t w = c_hi - c_lo;
                 bool replan = false;
-                if (est > 1.15 * kX && w > 1) {
+                if (est > KK_SLAB_ACCEPT * kX && w > 1) {
                     W = imax64(1, static_cast<int64_t>(w * (0.9 * kX / est)));
                     replan = true;
+                    PROF_COUNT(12, 1);
                 } else if (est < 0.2 * kX && c_hi < C_hi) {
                     W = static_cast<int64_t>(w * fmin(8.0, 0.6 * kX / fmax(est, 1.0))) + 1;
                     replan = true;
+                    PROF_COUNT(13, 1);
                 }
                 if (replan) {
                     ++replans;
@@ -482,55 +496,67 @@ __global__ void __launch_bounds__(kWarps * 32, KK_SLAB_CTAS) numeric_wslab_kerne
                 }
             };
             if (nr > 0) {
+                // window producer: batch pb at window offset pw0 (pn made, the
+                // run data of the batch after it in flight); the consumer
+                // keeps two mapped windows ahead of the one it folds
                 int64_t s0, s1, s2;
                 int32_t l0, l1, l2;
                 double a0, a1, a2;
                 fetch(0, s0, l0, a0);
                 fetch(32, s1, l1, a1);
                 fetch(64, s2, l2, a2);
-                Batch cur = make(0, s0, l0, a0);
-                Batch nxt = make(32, s1, l1, a1);
-                int32_t cr0 = 0, cw0 = 0;
-                int32_t key, nkey = -1;
-                double bv, a, nbv = 0.0, na = 0.0;
-                bool single, nsingle = true;
-                map(cur, 0, key, bv, a, single);
-                for (;;) {
-                    bool next_in_cur = false, has_next = true;
-                    if (cw0 + 32 < cur.total) {
-                        map(cur, cw0 + 32, nkey, nbv, na, nsingle);
-                        next_in_cur = true;
-                    } else if (cr0 + 32 < nr) {
-                        map(nxt, 0, nkey, nbv, na, nsingle);
-                    } else {
-                        has_next = false;
+                Batch pb = make(0, s0, l0, a0);
+                Batch pn = make(32, s1, l1, a1);
+                int32_t pr0 = 0, pw0 = 0;
+                auto produce = [&](int32_t& k, double& b, double& av, bool& sg) -> bool {
+                    if (pw0 >= pb.total) {
+                        if (pr0 + 32 >= nr)
+                            return false;
+                        pr0 += 32;
+                        pw0 = 0;
+                        pb = pn; // not mapped yet (rank 0)
+                        pn = make(pr0 + 32, s2, l2, a2);
+                        fetch(pr0 + 64, s2, l2, a2);
                     }
-                    const bool valid = cw0 + lane < cur.total;
-                    const double v = __dmul_rn(a, bv);
-                    low = low || (valid && key < c_lo);
-                    if (single)
-                        fold<true>(valid, key, v, tab, nk, lane);
+                    map(pb, pw0, k, b, av, sg); // key -1 past the batch's products
+                    pw0 += 32;
+                    return true;
+                };
+                // ring of kDepth + 1 windows: [0] is folded, [1..kDepth] in flight
+                int32_t wk[kDepth + 1];
+                double wb[kDepth + 1], wx[kDepth + 1];
+                bool wg[kDepth + 1], wh[kDepth + 1];
+#pragma unroll
+                for (int u = 0; u < kDepth; ++u) {
+                    wk[u] = -1;
+                    wb[u] = wx[u] = 0.0;
+                    wg[u] = true;
+                    wh[u] = (u == 0 || wh[u - 1]) && produce(wk[u], wb[u], wx[u], wg[u]);
+                }
+                while (wh[0]) {
+                    wk[kDepth] = -1;
+                    wb[kDepth] = wx[kDepth] = 0.0;
+                    wg[kDepth] = true;
+                    wh[kDepth] = wh[kDepth - 1] && produce(wk[kDepth], wb[kDepth], wx[kDepth], wg[kDepth]);
+                    const bool valid = wk[0] >= 0;
+                    const double v = __dmul_rn(wx[0], wb[0]);
+                    low = low || (valid && wk[0] < c_lo);
+                    if (wg[0])
+                        fold<true>(valid, wk[0], v, tab, nk, lane);
                     else
-                        fold<false>(valid, key, v, tab, nk, lane);
+                        fold<false>(valid, wk[0], v, tab, nk, lane);
                     if (nk > kTWMax) {
                         ovf = true;
                         break;
                     }
-                    if (!has_next)
-                        break;
-                    if (next_in_cur) {
-                        cw0 += 32;
-                    } else {
-                        cr0 += 32;
-                        cw0 = 0;
-                        cur = nxt; // its window 0 is already mapped (rank advanced)
-                        nxt = make(cr0 + 32, s2, l2, a2);
-                        fetch(cr0 + 64, s2, l2, a2);
+#pragma unroll
+                    for (int u = 0; u < kDepth; ++u) {
+                        wh[u] = wh[u + 1];
+                        wk[u] = wk[u + 1];
+                        wb[u] = wb[u + 1];
+                        wx[u] = wx[u + 1];
+                        wg[u] = wg[u + 1];
                     }
-                    key = nkey;
-                    bv = nbv;
-                    a = na;
-                    single = nsingle;
                 }
             }
             PROF_MARK(2);

@@ -28,7 +28,8 @@ e1.record()
 torch.cuda.synchronize()
 f(buf, 0)
 names = ["cursor_init_cyc", "plan_cyc", "fold_cyc", "emit_cyc", "", "", "", "",
-         "slabs", "products", "replans", "aborts", "", "", "", ""]
+         "slabs", "products", "replans", "aborts", "replans_narrower", "replans_wider", "runs_planned",
+         "entries_planned"]
 print(f"s{scale} numeric {e0.elapsed_time(e1):.2f} ms heavy_path={h.heavy_path}")
 for n, v in zip(names, buf):
     if n:
