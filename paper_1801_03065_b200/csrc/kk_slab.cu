@@ -220,9 +220,13 @@ __device__ __forceinline__ WarpScratch warp_scratch(unsigned char* base, int64_t
 
 // shared memory per warp: the table and the slots its keys occupy (for an
 // O(keys) emission)
+constexpr int kQueue = 64; // plan queue ring (entries with a run in the slab)
 struct __align__(16) WarpSmem {
     int32_t keys[kTW];
     double vals[kTW];
+    int64_t qpos[kQueue];
+    int32_t qrem[kQueue];
+    int32_t qp[kQueue];
     uint16_t used[kTWMax + 32];
 };
 
@@ -349,63 +353,72 @@ __global__ void __launch_bounds__(kWarps * 32, KK_SLAB_CTAS) numeric_wslab_kerne
         int replans = 0;
         while (c_lo < C_hi && !bad) {
             const int64_t c_hi = W >= C_hi - c_lo ? C_hi : c_lo + W;
-            // ---- plan: runs of every A entry in [c_lo, c_hi), two groups of
-            //      32 entries per step (independent loads in flight) ----
+            // ---- plan: runs of every A entry in [c_lo, c_hi).  Cursors are
+            //      scanned 32 at a time (two groups ahead in flight); the
+            //      entries with a run here are queued in A order, and run ends
+            //      are searched 32 queued entries at a time, every lane busy ----
             int64_t prods = 0;
             int32_t nr = 0;
-            // the next step's cursors are loaded while this step probes B
-            Cursor fa{0, 0, INT_MAX}, fb{0, 0, INT_MAX};
+            int qh = 0, qn = 0; // queue ring [qh, qh + qn) mod kQueue
+            auto search = [&](int cnt) {
+                const bool act = lane < cnt;
+                int64_t pos = 0;
+                int32_t rem = 0, p = 0;
+                if (act) {
+                    const int q = (qh + lane) & (kQueue - 1);
+                    pos = tab.qpos[q];
+                    rem = tab.qrem[q];
+                    p = tab.qp[q];
+                }
+                Probe16 P;
+                probe16(L.b_cols, pos, pos + rem, P);
+                const double av = act ? __ldg(L.a_vals + abeg + p) : 0.0;
+                if (act) {
+                    int32_t x = INT_MAX;
+                    const int64_t e = finish16(L.b_cols, pos, pos + rem, c_hi, P, &x);
+                    const int r = nr + lane;
+                    ws.rs[r] = pos;
+                    ws.ra[r] = av;
+                    ws.rl[r] = static_cast<int32_t>(e - pos);
+                    ws.rp[r] = p;
+                    ws.rnx[r] = x;
+                    prods += e - pos;
+                }
+                nr += cnt;
+                qh = (qh + cnt) & (kQueue - 1);
+                qn -= cnt;
+            };
+            Cursor f1{0, 0, INT_MAX}, f2{0, 0, INT_MAX};
             if (lane < d)
-                fa = ws.cur[lane];
+                f1 = ws.cur[lane];
             if (32 + lane < d)
-                fb = ws.cur[32 + lane];
-            for (int64_t p0 = 0; p0 < d; p0 += 64) {
-                const int64_t pa = p0 + lane, pb = p0 + 32 + lane;
-                const Cursor ca = fa, cb = fb;
-                fa = Cursor{0, 0, INT_MAX};
-                fb = Cursor{0, 0, INT_MAX};
-                if (pa + 64 < d)
-                    fa = ws.cur[pa + 64];
-                if (pb + 64 < d)
-                    fb = ws.cur[pb + 64];
-                const bool na = ca.nxt < c_hi, nb = cb.nxt < c_hi;
-                bad = bad || (na && ca.nxt < c_lo) || (nb && cb.nxt < c_lo); // an earlier run ended early: unsorted B row
-                int32_t xa = INT_MAX, xb = INT_MAX;
-                int64_t ea = 0, eb = 0;
-                double aa = 0.0, ab = 0.0;
-                Probe16 Pa, Pb; // both groups' first loads in flight before either is evaluated
-                probe16(L.b_cols, ca.pos, na ? ca.pos + ca.rem : ca.pos, Pa);
-                probe16(L.b_cols, cb.pos, nb ? cb.pos + cb.rem : cb.pos, Pb);
-                if (na)
-                    aa = __ldg(L.a_vals + abeg + pa);
-                if (nb)
-                    ab = __ldg(L.a_vals + abeg + pb);
-                if (na)
-                    ea = finish16(L.b_cols, ca.pos, ca.pos + ca.rem, c_hi, Pa, &xa);
-                if (nb)
-                    eb = finish16(L.b_cols, cb.pos, cb.pos + cb.rem, c_hi, Pb, &xb);
-                const uint32_t Ma = __ballot_sync(kFull, na), Mb = __ballot_sync(kFull, nb);
+                f2 = ws.cur[32 + lane];
+            for (int64_t p0 = 0; p0 < d; p0 += 32) {
+                const int64_t p = p0 + lane;
+                const Cursor c = f1;
+                f1 = f2;
+                f2 = Cursor{0, 0, INT_MAX};
+                if (p + 64 < d)
+                    f2 = ws.cur[p + 64];
+                const bool na = c.nxt < c_hi; // past-the-end lanes: nxt INT_MAX
+                bad = bad || (na && c.nxt < c_lo); // an earlier run ended early: unsorted B row
+                const uint32_t M = __ballot_sync(kFull, na);
                 if (na) {
-                    const int r = nr + __popc(Ma & lanemask_lt());
-                    ws.rs[r] = ca.pos;
-                    ws.ra[r] = aa;
-                    ws.rl[r] = static_cast<int32_t>(ea - ca.pos);
-                    ws.rp[r] = static_cast<int32_t>(pa);
-                    ws.rnx[r] = xa;
-                    prods += ea - ca.pos;
+                    const int q = (qh + qn + __popc(M & lanemask_lt())) & (kQueue - 1);
+                    tab.qpos[q] = c.pos;
+                    tab.qrem[q] = c.rem;
+                    tab.qp[q] = static_cast<int32_t>(p);
                 }
-                nr += __popc(Ma);
-                if (nb) {
-                    const int r = nr + __popc(Mb & lanemask_lt());
-                    ws.rs[r] = cb.pos;
-                    ws.ra[r] = ab;
-                    ws.rl[r] = static_cast<int32_t>(eb - cb.pos);
-                    ws.rp[r] = static_cast<int32_t>(pb);
-                    ws.rnx[r] = xb;
-                    prods += eb - cb.pos;
+                qn += __popc(M);
+                __syncwarp();
+                if (qn >= 32) {
+                    search(32);
+                    __syncwarp();
                 }
-                nr += __popc(Mb);
             }
+            if (qn > 0)
+                search(qn);
+            __syncwarp();
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1)
                 prods += __shfl_xor_sync(kFull, prods, o);
