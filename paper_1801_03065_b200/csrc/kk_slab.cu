@@ -56,10 +56,10 @@ constexpr int kWarps = 8;                          // independent warps per CTA
 constexpr int kTW = 1 << KK_SLAB_LOG2_TW;          // table slots per warp
 constexpr int kTWMax = kTW * 3 / 4;                // keys before a slab is abandoned
 #ifndef KK_SLAB_XFRAC
-#define KK_SLAB_XFRAC 500 // target keys per slab, per 1024 table slots
+#define KK_SLAB_XFRAC 450 // target keys per slab, per 1024 table slots
 #endif
 #ifndef KK_SLAB_ACCEPT
-#define KK_SLAB_ACCEPT 1.45 // a planned slab predicted above ACCEPT * kX keys is re-planned narrower
+#define KK_SLAB_ACCEPT 1.6 // a planned slab predicted above ACCEPT * kX keys is re-planned narrower
 #endif
 constexpr int kX = kTW * KK_SLAB_XFRAC / 1024;     // target distinct keys per slab
 constexpr double kSplitWork = 4e8;  // A-row length x row size per part
