@@ -45,7 +45,7 @@ def _stale(target: str, sources: list[str]) -> bool:
 
 
 def build_kkspgemm(force: bool = False, verbose: bool = False) -> str:
-    srcs = [os.path.join(CSRC, f) for f in ("kk_api.cu", "kk_kernels.cu", "kk_fast.cu", "kk_heavy.cu", "kk_slab.cu", "kk_replay.cu")]
+    srcs = [os.path.join(CSRC, f) for f in ("kk_api.cu", "kk_kernels.cu", "kk_fast.cu", "kk_heavy.cu", "kk_slab.cu", "kk_replay.cu", "kk_tiny.cu")]
     deps = srcs + [os.path.join(CSRC, f) for f in ("kk_device.cuh", "kk_internal.h")] + [
         os.path.join(ROOT, "include", "kkspgemm.h")]
     if force or _stale(LIB, deps):

@@ -112,6 +112,7 @@ int host_bucket(unsigned long long x)
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kWarpSmemMax = 48 * 1024; // L1 accumulator budget per warp
+constexpr double kTinyMaxAvgArow = 8.0;        // thread-per-row classes only for short A rows
 constexpr int32_t kHeavySymWords = 49152;     // 192 KB dense bitmap per CTA (heavy symbolic)
 constexpr int32_t kHeavyBucketKeys = 256;     // numeric heavy rows: ~distinct columns per hashed bucket
 constexpr int32_t kHeavyMaxBuckets = 1536;    // buckets per row (shared-memory histogram bound)
@@ -207,6 +208,7 @@ struct PhaseClass {
     TabLayout lay;
     bool l2 = false;
     bool fast = false;
+    bool tiny = false; // a thread per row (kk_tiny.cu)
     int wpb = 8;
     int grid = 0;
     int64_t count = 0;
@@ -327,7 +329,7 @@ L2Spec plan_l2(int acc, int variant, int64_t s_true, int32_t domain, int64_t row
 // flops/collapse_divisor, engine.cpp:410-411, with 2x headroom).
 PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsigned long long* hist,
                      int64_t umax, const spg_config& cfg, bool fast = false, int opt_div = 0,
-                     bool short_rows = false)
+                     bool short_rows = false, double avg_a_row = 0.0)
 {
     PhasePlan P;
     P.acc = acc;
@@ -360,8 +362,13 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
         if (layout_of(c).bytes <= kWarpSmemMax)
             l1caps.push_back(c);
 
-    // bucket -> class
-    std::vector<int64_t> cls_count(l1caps.size() + 1, 0);
+    // bucket -> class: [l1caps..., L2, tiny]; rows whose bound (exact row size
+    // for the numeric phase, flops / compressed flops for the symbolic one)
+    // is at most kTinyKeys run a thread per row (kk_tiny.cu)
+    // (only when A rows are short: a thread walks its A row's entries serially)
+    const bool tiny_ok = fast && l1cap >= 32 && avg_a_row <= kTinyMaxAvgArow && getenv("KK_NO_TINY") == nullptr;
+    const int tiny_c = static_cast<int>(l1caps.size()) + 1;
+    std::vector<int64_t> cls_count(l1caps.size() + 2, 0);
     int8_t bc[64];
     for (int b = 0; b < 64; ++b) {
         bc[b] = -1;
@@ -369,6 +376,11 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
         if (be == 0)
             continue;
         int64_t need = std::min<int64_t>(int64_t{1} << (be - 1), std::max<int32_t>(domain, 1));
+        if (tiny_ok && need <= (variant == kVarNumeric ? kTinyKeys : kTinySymKeys)) {
+            bc[b] = static_cast<int8_t>(tiny_c);
+            cls_count[tiny_c] += static_cast<int64_t>(hist[b]);
+            continue;
+        }
         if (fast && opt_div > 0) {
             const int64_t est = std::max<int64_t>(32, ceil_pow2_i((2 * need + opt_div - 1) / opt_div));
             if (est < need) {
@@ -396,7 +408,10 @@ PhasePlan plan_phase(int acc, bool flat, int variant, int32_t domain, const unsi
         pc.off = off;
         off += pc.count;
         pc.l2 = c == l1caps.size();
-        if (!pc.l2) {
+        pc.tiny = static_cast<int>(c) == tiny_c;
+        if (pc.tiny) {
+            pc.fast = true;
+        } else if (!pc.l2) {
             pc.fast = fast;
             pc.lay = layout_of(l1caps[c]);
             pc.wpb = static_cast<int>(std::clamp<uint64_t>(kCtaSmem / pc.lay.bytes, 1, 8));
@@ -657,7 +672,8 @@ void build_numeric_plan(spg_handle* h, cudaStream_t st, const int64_t* a_rowptr 
     } else if (acc == kAccLP && cfg.l1_capacity <= 0) {
         fast = true; // forced LP: same algorithms, fast kernels
     }
-    h->num = plan_phase(acc, flat, kVarNumeric, h->info.k, h->size_hist.hist, h->info.max_row_size, cfg, fast, 0);
+    h->num = plan_phase(acc, flat, kVarNumeric, h->info.k, h->size_hist.hist, h->info.max_row_size, cfg, fast, 0,
+                        false, h->info.m > 0 ? static_cast<double>(h->info.nnz_a) / h->info.m : 0.0);
     // Auto: rows beyond the warp tables take the bucketed CTA path (kk_heavy.cu)
     // when a row's distinct columns fit the hashed buckets and its products
     // fit 32-bit staging offsets
@@ -1079,7 +1095,8 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         const bool short_rows = I.flops.avg_row_flops < cfg.avg_flops_cutoff;
         const PhasePlan S = plan_phase(sfast ? kAccLP : sacc, sfast ? true : sflat, variant, domain,
                                        apply ? htot->hist_cf : htot->hist_f, raw_bound, cfg, sfast,
-                                       sfast ? std::max(cfg.collapse_divisor, 1) : 0, short_rows);
+                                       sfast ? std::max(cfg.collapse_divisor, 1) : 0, short_rows,
+                                       m > 0 ? static_cast<double>(I.nnz_a) / m : 0.0);
         cuda_check(cudaMemsetAsync(h->d_rowptr, 0, sizeof(int64_t) * (int64_t{m} + 1), st), "memset");
         int32_t* d_list = nullptr;
         if (S.need_list) {
@@ -1130,6 +1147,9 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
                 L.pool = PoolDesc{spool.base, S.l2.chunk_bytes, S.l2.num_chunks, S.l2.pool_mode, spool.states};
                 cuda_check(launch_row_kernel(L, S.fast ? kAccLP : S.acc, S.fast ? false : S.flat, S.variant, st),
                            "symbolic L2 kernel");
+            } else if (pc.tiny) {
+                cuda_check(launch_symbolic_tiny(L, S.variant == kVarSymCompressed, d_retry_cnt, d_retry, st),
+                           "symbolic tiny kernel");
             } else if (pc.fast) {
                 cuda_check(launch_symbolic_fast(L, S.variant == kVarSymCompressed, S.short_rows, d_retry_cnt, d_retry, st),
                            "symbolic kernel");
@@ -1346,6 +1366,8 @@ static int numeric_impl(spg_handle_t h, const spg_csr* a, const spg_csr* b, int3
                                   h->num_pool.states};
                 cuda_check(launch_row_kernel(L, P.fast ? kAccLP : P.acc, P.fast ? false : P.flat, kVarNumeric, st),
                            "numeric L2 kernel");
+            } else if (pc.tiny) {
+                cuda_check(launch_numeric_tiny(L, st), "numeric tiny kernel");
             } else if (pc.fast) {
                 cuda_check(P.flat ? launch_numeric_flat_fast(L, st) : launch_numeric_fast(L, st), "numeric kernel");
             } else {

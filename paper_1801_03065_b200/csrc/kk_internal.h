@@ -126,6 +126,13 @@ cudaError_t launch_numeric_fast(const RowLaunch& L, cudaStream_t st);
 int numeric_fast_blocks_per_sm(int wpb, size_t smem);
 cudaError_t launch_numeric_flat_fast(const RowLaunch& L, cudaStream_t st);
 int numeric_flat_fast_blocks_per_sm(int wpb, size_t smem);
+// rows of at most kTinyKeys (numeric) / kTinySymKeys (symbolic) keys, a
+// thread per row (kk_tiny.cu)
+constexpr int kTinyKeys = 16;
+constexpr int kTinySymKeys = 32;
+cudaError_t launch_numeric_tiny(const RowLaunch& L, cudaStream_t st);
+cudaError_t launch_symbolic_tiny(const RowLaunch& L, bool compressed, unsigned long long* retry_count,
+                                 int32_t* retry_list, cudaStream_t st);
 cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, bool pipe, unsigned long long* retry_count,
                                  int32_t* retry_list, cudaStream_t st);
 int symbolic_fast_blocks_per_sm(bool compressed, bool pipe, int wpb, size_t smem);

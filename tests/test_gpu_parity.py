@@ -792,6 +792,53 @@ def test_short_and_long_rows_bitwise(kk, oracle):
     assert np.array_equal(vals.cpu().numpy().view(np.int64), full.values.view(np.int64))
 
 
+def test_tiny_rows_thread_per_row(kk, oracle, monkeypatch):
+    """Short A rows whose C rows hold <= 16 keys run a thread per row
+    (kk_tiny.cu): raw first-touch order and value bits (specials included)
+    equal the reference's and the warp kernels' (KK_NO_TINY=1), through
+    spg_numeric_rows too; a reused handle whose new B changes the rows' key
+    counts is reported (engine.cpp:238-245)."""
+    import torch
+    rng = np.random.default_rng(63)
+    m, n, k = 5000, 3000, 4000
+    a = random_csr(rng, m, n, 4.0 / n)
+    b = random_csr(rng, n, k, 3.0 / k)
+    specials = np.array([np.inf, -np.inf, np.nan, -0.0, 0.0, 5e-324, 1.7e308])
+    for x in (a, b):
+        pick = rng.choice(x.nnz(), x.nnz() // 10, replace=False)
+        x.values[pick] = rng.choice(specials, len(pick))
+    ro = oracle.symbolic_row_offsets(a, b)
+    assert (np.diff(ro) <= 16).mean() > 0.5 and np.diff(ro).max() > 16  # tiny and warp classes mixed
+    cols, vals = oracle.numeric(a, b, ro)
+    nan = np.isnan(vals)
+    res = kk.multiply(a, b).c.to_host()
+    monkeypatch.setenv("KK_NO_TINY", "1")
+    warp = kk.multiply(a, b).c.to_host()
+    monkeypatch.delenv("KK_NO_TINY")
+    for c in (res, warp):
+        assert np.array_equal(c.row_offsets, ro)
+        assert np.array_equal(c.col_indices, cols)
+        assert np.array_equal(np.isnan(c.values), nan)
+        assert np.array_equal(c.values[~nan].view(np.int64), vals[~nan].view(np.int64))
+    # row blocks
+    da, db = a.to_device(), b.to_device()
+    h = kk.symbolic(da, db)
+    ccols = torch.full((h.nnz_c(),), -3, dtype=torch.int32, device="cuda")
+    cvals = torch.zeros(h.nnz_c(), dtype=torch.float64, device="cuda")
+    for r0, r1 in ((0, 1700), (1700, 1701), (1701, m)):
+        kk.numeric_rows(da, db, h, r0, r1, ccols, cvals)
+    assert np.array_equal(ccols.cpu().numpy(), cols)
+    # structure changes under a reused handle (same nnz, B's columns moved):
+    # rows of C with more or fewer keys than the structure are reported
+    h = kk.symbolic(a, b)
+    b2 = kk.CsrMatrix(b.num_rows, b.num_cols, b.row_offsets, b.col_indices.copy(), b.values, False)
+    for i in range(b2.num_rows):
+        lo, hi = b2.row_offsets[i], b2.row_offsets[i + 1]
+        b2.col_indices[lo:hi] = (np.arange(hi - lo) * 7 + i) % 40
+    with pytest.raises(kk.InternalError):
+        kk.numeric(a, b2, h, kk.PhaseStats())
+
+
 def test_numeric_reuse_is_graph_capturable(kk, oracle):
     """Once a handle replays (third numeric pass on), spg_numeric is fully
     stream-ordered: the reuse loop can be captured in a CUDA graph and replayed
