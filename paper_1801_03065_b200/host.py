@@ -207,7 +207,10 @@ def multiply_host(a: PinnedCsr, b: Optional[PinnedCsr] = None, cfg: Optional[Spg
     nnz_c = h.nnz_c()
     m = hi - lo
     c_ro = h.device_row_offsets(main)
-    ro_host = h.c_row_offsets  # block boundaries of C (one small copy)
+    # C's offsets at the block boundaries only (a gather of len(cuts) values,
+    # not a pageable copy of all m + 1 offsets)
+    bidx = torch.tensor([c - lo for c in cuts], dtype=torch.int64, device=dev)
+    ro_cut = dict(zip((c - lo for c in cuts), c_ro.index_select(0, bidx).cpu().tolist()))
     mark("symbolic done", main)
     if out is not None and out[0].numel() >= m + 1 and out[1].numel() >= nnz_c and out[2].numel() >= nnz_c:
         o_ro, o_ci, o_v = out
@@ -233,7 +236,7 @@ def multiply_host(a: PinnedCsr, b: Optional[PinnedCsr] = None, cfg: Optional[Spg
         done = torch.cuda.Event()
         done.record(main)
         side.wait_event(done)
-        e0, e1 = int(ro_host[b0]), int(ro_host[b1])
+        e0, e1 = ro_cut[b0], ro_cut[b1]
         if e1 > e0:
             with torch.cuda.stream(side):
                 o_ci[e0:e1].copy_(d_ci[e0:e1], non_blocking=True)
