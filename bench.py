@@ -229,6 +229,10 @@ def cpu_baseline(cfg, mats, full_flops):
 
 
 class Clocks:
+    """nvidia-smi clock / throttle-reason samples (100 ms) over the timed
+    region.  The sampler is started first and the region begins only once it
+    reports (its start-up takes longer than a short timed region); samples
+    from the start-up wait are dropped."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -236,24 +240,41 @@ class Clocks:
     def __init__(self, dev: int):
         self.dev = dev
         self.p = None
+        self.lines = []
+        self.t0 = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append((time.perf_counter(), line))
 
     def __enter__(self):
+        import threading
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+            deadline = time.perf_counter() + 5.0
+            while not self.lines and time.perf_counter() < deadline:
+                time.sleep(0.01)
         except Exception:
             self.p = None
+        self.t0 = time.perf_counter()
         return self
 
     def __exit__(self, *exc):
         self.rows = []
         if self.p is None:
             return
-        time.sleep(0.25)
+        time.sleep(0.15)  # one more sample after the region
         self.p.terminate()
-        out, _ = self.p.communicate(timeout=5)
-        for line in out.strip().splitlines():
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            pass
+        for t, line in list(self.lines):
+            if t < self.t0:
+                continue
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 6:
                 self.rows.append(parts)

@@ -582,6 +582,7 @@ int numeric_flat_fast_blocks_per_sm(int wpb, size_t smem)
 // ---------------------------------------------------------------------------
 // symbolic: order-free union, LP table of {key, word} slots
 // ---------------------------------------------------------------------------
+constexpr int kSymMaxProbe = 32;
 template <bool kCompressed, bool kPipe>
 __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, unsigned long long* retry_count,
                                                             int32_t* retry_list)
@@ -609,14 +610,15 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
 
     // one chunk of <= 32 A entries of the current row, B-row descriptors in registers
     auto chunk = [&](int na, int64_t bb, int32_t bl) {
-            // probe / claim / OR one (key, word); false only when the table is
-            // full (the row is then handed to the exact-size path).  Rows past
-            // the optimistic key count but within the table complete here.
+            // probe / claim / OR one (key, word); false when the probe sequence
+            // exceeds kSymMaxProbe slots (the table is over-full: the row's size
+            // was underestimated) — the row is then handed to the exact-size
+            // path.  No per-window claim count is needed.
             auto insert = [&](int32_t key, uint32_t word) -> bool {
                 if (key == kEmpty)
                     return true;
                 uint32_t s = loc_hash(key, pshift);
-                for (int probes = 0; probes < T; ++probes) {
+                for (int probes = 0; probes < kSymMaxProbe && probes < T; ++probes) {
                     const int32_t k = keys[s];
                     bool hit = k == key;
                     if (k == kEmpty) {
