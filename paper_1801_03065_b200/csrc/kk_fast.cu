@@ -410,11 +410,14 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
 
     // One row's accumulation over a chunk of <= 32 A entries whose B-row
     // descriptors (bb, bl) and A values are already in registers.
-    auto chunk = [&](int64_t bb, int32_t bl, double av, int32_t cap, int32_t& cnt) {
+    auto chunk = [&](int64_t bb, int32_t bl, double av, int32_t cap, int32_t& cnt, FlatMap<true>* pre = nullptr) {
         // flattened prefix of this chunk's B-row lengths (32-bit: one chunk of
         // a flat-scheme row never holds 2^31 products)
         FlatMap<true> fm;
-        fm.init(bb, bl, av, lane, scratch);
+        if (pre)
+            fm = *pre;
+        else
+            fm.init(bb, bl, av, lane, scratch);
         const int32_t total = fm.total;
         for (int32_t w0 = 0; w0 < total; w0 += 32) {
             const int32_t t = w0 + lane;
@@ -431,6 +434,46 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
                 v = __dmul_rn(a, ldg_keep(L.b_vals + q, pol));
             }
             num_window(valid, key, v, keys, vals, slot_of, tmask, shift, cap, cnt, lane);
+        }
+    };
+    // A row whose products fit one window needs no table: the window's key
+    // groups (in lane = product order) are the row's keys, their leaders in
+    // lane order the first-touch positions, each group folded left to right.
+    auto direct = [&](const FlatMap<true>& fm0, int64_t cbase, int32_t cap) {
+        FlatMap<true> fm = fm0;
+        int32_t e;
+        int64_t base;
+        double a;
+        fm.window(0, lane, e, base, a);
+        const bool valid = lane < fm.total;
+        int32_t key = 0;
+        double v = 0.0;
+        if (valid) {
+            const int64_t q = base + (lane - e);
+            key = ldg_keep(L.b_cols + q, pol);
+            v = __dmul_rn(a, ldg_keep(L.b_vals + q, pol));
+        }
+        const uint32_t grp = __match_any_sync(kFull, valid ? key : (-1 - lane));
+        const bool leader = valid && (__ffs(grp) - 1) == lane;
+        double acc = v;
+        uint32_t rest = leader ? (grp & (grp - 1)) : 0u;
+        const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(rest)));
+        for (int rr = 0; rr < rounds; ++rr) {
+            const int src = rest ? __ffs(rest) - 1 : lane;
+            const double xv = __shfl_sync(kFull, v, src);
+            if (rest) {
+                acc = __dadd_rn(acc, xv);
+                rest &= rest - 1;
+            }
+        }
+        const uint32_t lm = __ballot_sync(kFull, leader);
+        const int32_t n = __popc(lm);
+        if (n != cap && lane == 0)
+            raise_error(L.ctr, n < cap ? kDevRowShort : kDevRowOverflow);
+        const int32_t pos = __popc(lm & lanemask_lt());
+        if (leader && pos < cap) {
+            st_stream(L.c_cols + cbase + pos, key);
+            st_stream(L.c_vals + cbase + pos, acc);
         }
     };
     auto finish = [&](int64_t cbase, int32_t cap, int32_t cnt) {
@@ -504,7 +547,13 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
             const int32_t cap = __shfl_sync(kFull, rcap, q);
             int32_t cnt = 0;
             if (len <= 32) {
-                chunk(bb, bl, av, cap, cnt);
+                FlatMap<true> fm;
+                fm.init(bb, bl, av, lane, scratch);
+                if (fm.total <= 32) {
+                    direct(fm, cb, cap);
+                    return;
+                }
+                chunk(bb, bl, av, cap, cnt, &fm);
             } else {
                 const int64_t ab = __shfl_sync(kFull, rab, q);
                 for (int64_t p0 = ab; p0 < ab + len; p0 += 32) {
@@ -710,6 +759,50 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                 }
             }
     };
+    // A row of at most 32 (key, word) pairs needs no table: the window's key
+    // groups are its distinct keys (size = their count, or the popcount of
+    // each group's OR).  Returns -1 when the row has more pairs.
+    auto direct_size = [&](int64_t bb, int32_t bl) -> int64_t {
+        const int32_t csum = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<unsigned>(bl)));
+        if (csum > 32)
+            return -1;
+        FlatMap<false> fm;
+        fm.init(bb, bl, 0.0, lane, scratch);
+        int32_t e;
+        int64_t base;
+        double a_unused;
+        fm.window(0, lane, e, base, a_unused);
+        const bool valid = lane < csum;
+        int32_t key = 0;
+        uint32_t word = 0u;
+        if (valid) {
+            if constexpr (kCompressed) {
+                const int2 pr = __ldg(cpair + base + (lane - e));
+                key = pr.x;
+                word = static_cast<uint32_t>(pr.y);
+            } else {
+                key = __ldg(L.b_cols + base + (lane - e));
+            }
+        }
+        const uint32_t grp = __match_any_sync(kFull, valid ? key : (-1 - lane));
+        const bool leader = valid && (__ffs(grp) - 1) == lane;
+        if constexpr (!kCompressed) {
+            return __popc(__ballot_sync(kFull, leader));
+        } else {
+            uint32_t orv = word;
+            uint32_t rest = leader ? (grp & (grp - 1)) : 0u;
+            const int rounds = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(rest)));
+            for (int rr = 0; rr < rounds; ++rr) {
+                const int src = rest ? __ffs(rest) - 1 : lane;
+                const uint32_t x = __shfl_sync(kFull, word, src);
+                if (rest) {
+                    orv |= x;
+                    rest &= rest - 1;
+                }
+            }
+            return __reduce_add_sync(kFull, leader ? static_cast<unsigned>(__popc(orv)) : 0u);
+        }
+    };
     // size of the finished row (or its hand-off to the L2 path); table reset
     auto finish = [&](int32_t i) {
         __syncwarp();
@@ -748,9 +841,18 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                     bb = __ldg(b_rowptr + j);
                     bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
                 }
+                if (aend - abeg <= 32) {
+                    const int64_t sz = direct_size(bb, bl);
+                    if (sz >= 0) {
+                        if (lane == 0)
+                            L.sym_sizes[i] = sz;
+                        goto next_row;
+                    }
+                }
                 chunk(na, bb, bl);
             }
             finish(i);
+        next_row:;
         }
         return;
     }
@@ -796,6 +898,12 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
             const int32_t len = __shfl_sync(kFull, ralen, q);
             const int32_t i = __shfl_sync(kFull, rrow, q);
             if (len <= 32) {
+                const int64_t sz = direct_size(bb, bl);
+                if (sz >= 0) {
+                    if (lane == 0)
+                        L.sym_sizes[i] = sz;
+                    return;
+                }
                 chunk(len, bb, bl);
             } else {
                 const int64_t ab = __shfl_sync(kFull, rab, q);
