@@ -273,7 +273,7 @@ static_assert(sizeof(FlatScratch) == 640, "layouts reserve 640 B (symbolic) / 76
 
 template <bool kWithA>
 struct FlatMap {
-    int64_t cbase;  // compacted: lane c holds the B-row base of the c-th non-empty segment
+    int64_t cbase;  // compacted: lane c holds B-row base - start of the c-th non-empty segment
     double ca;      // ... its A value
     int32_t cexcl;  // ... its start in the flattened index space
     int32_t nne;    // non-empty segments
@@ -308,8 +308,8 @@ struct FlatMap {
         ca = 0.0;
         cexcl = 0;
         if (lane < nne) {
-            cbase = sc->base[lane];
             cexcl = sc->excl[lane];
+            cbase = sc->base[lane] - cexcl; // product t of the segment: B position cbase + t
             if constexpr (kWithA)
                 ca = sc->a[lane];
         }
@@ -317,15 +317,15 @@ struct FlatMap {
         rank = 0;
     }
 
-    // segment data of this lane's product in window [w0, w0+32); advances rank
-    __device__ __forceinline__ void window(int32_t w0, int lane, int32_t& e, int64_t& base, double& a)
+    // segment data of this lane's product in window [w0, w0+32): the B
+    // position of product w0 + lane is pos0 + lane; advances rank
+    __device__ __forceinline__ void window(int32_t w0, int lane, int64_t& pos0, double& a)
     {
         const uint32_t bit = (lane < nne && cexcl >= w0 && cexcl < w0 + 32) ? (1u << (cexcl - w0)) : 0u;
         const uint32_t M = __reduce_or_sync(kFull, bit);
         int seg = rank + __popc(M & ((2u << lane) - 1u)) - 1;
         seg = seg < 0 ? 0 : (seg > 31 ? 31 : seg);
-        e = __shfl_sync(kFull, cexcl, seg);
-        base = __shfl_sync(kFull, cbase, seg);
+        pos0 = __shfl_sync(kFull, cbase, seg) + w0;
         if constexpr (kWithA)
             a = __shfl_sync(kFull, ca, seg);
         rank += __popc(M);
@@ -421,15 +421,14 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
         const int32_t total = fm.total;
         for (int32_t w0 = 0; w0 < total; w0 += 32) {
             const int32_t t = w0 + lane;
-            int32_t e;
-            int64_t base;
+            int64_t pos0;
             double a;
-            fm.window(w0, lane, e, base, a);
+            fm.window(w0, lane, pos0, a);
             const bool valid = t < total;
             int32_t key = 0;
             double v = 0.0;
             if (valid) {
-                const int64_t q = base + (t - e);
+                const int64_t q = pos0 + lane;
                 key = ldg_keep(L.b_cols + q, pol);
                 v = __dmul_rn(a, ldg_keep(L.b_vals + q, pol));
             }
@@ -441,15 +440,14 @@ __global__ void __launch_bounds__(256) numeric_lp_flat_kernel(const RowLaunch L)
     // lane order the first-touch positions, each group folded left to right.
     auto direct = [&](const FlatMap<true>& fm0, int64_t cbase, int32_t cap) {
         FlatMap<true> fm = fm0;
-        int32_t e;
-        int64_t base;
+        int64_t pos0;
         double a;
-        fm.window(0, lane, e, base, a);
+        fm.window(0, lane, pos0, a);
         const bool valid = lane < fm.total;
         int32_t key = 0;
         double v = 0.0;
         if (valid) {
-            const int64_t q = base + (lane - e);
+            const int64_t q = pos0 + lane;
             key = ldg_keep(L.b_cols + q, pol);
             v = __dmul_rn(a, ldg_keep(L.b_vals + q, pol));
         }
@@ -647,6 +645,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
     const int T = L.lay.T;
     const uint32_t tmask = static_cast<uint32_t>(T - 1);
     const int pshift = L.lay.shift;
+    const int maxp = T < kSymMaxProbe ? T : kSymMaxProbe;
     for (int t = lane; t < T; t += 32) {
         keys[t] = kEmpty;
         words[t] = 0u;
@@ -667,7 +666,7 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
                 if (key == kEmpty)
                     return true;
                 uint32_t s = loc_hash(key, pshift);
-                for (int probes = 0; probes < kSymMaxProbe && probes < T; ++probes) {
+                for (int probes = 0; probes < maxp; ++probes) {
                     const int32_t k = keys[s];
                     bool hit = k == key;
                     if (k == kEmpty) {
@@ -736,14 +735,13 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
             // window w0's (key, word) are loaded one window ahead
             auto fetch = [&](int32_t w0, int32_t& key, uint32_t& word) {
                 const int32_t t = w0 + lane;
-                int32_t e;
-                int64_t base;
+                int64_t pos0;
                 double a_unused;
-                fm.window(w0, lane, e, base, a_unused);
+                fm.window(w0, lane, pos0, a_unused);
                 key = kEmpty;
                 word = 0u;
                 if (t < total)
-                    load(base + (t - e), key, word);
+                    load(pos0 + lane, key, word);
             };
             int32_t nkey;
             uint32_t nword;
@@ -768,20 +766,19 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
             return -1;
         FlatMap<false> fm;
         fm.init(bb, bl, 0.0, lane, scratch);
-        int32_t e;
-        int64_t base;
+        int64_t pos0;
         double a_unused;
-        fm.window(0, lane, e, base, a_unused);
+        fm.window(0, lane, pos0, a_unused);
         const bool valid = lane < csum;
         int32_t key = 0;
         uint32_t word = 0u;
         if (valid) {
             if constexpr (kCompressed) {
-                const int2 pr = __ldg(cpair + base + (lane - e));
+                const int2 pr = __ldg(cpair + pos0 + lane);
                 key = pr.x;
                 word = static_cast<uint32_t>(pr.y);
             } else {
-                key = __ldg(L.b_cols + base + (lane - e));
+                key = __ldg(L.b_cols + pos0 + lane);
             }
         }
         const uint32_t grp = __match_any_sync(kFull, valid ? key : (-1 - lane));
