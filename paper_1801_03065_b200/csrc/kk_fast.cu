@@ -851,97 +851,98 @@ __global__ void __launch_bounds__(256) symbolic_flat_kernel(const RowLaunch L, u
             finish(i);
         next_row:;
         }
-        return;
-    }
-    // Short rows: taken 32 at a time and their dependent loads pipelined
-    // across rows (A entries two rows ahead, B-row descriptors one ahead;
-    // three register sets unrolled by three), as in numeric_lp_flat_kernel.
-    for (int64_t r0 = ((int64_t)blockIdx.x * L.wpb + wib) * 32; r0 < L.nrows; r0 += nwarps * 32) {
-        const int nr = static_cast<int>(L.nrows - r0 < 32 ? L.nrows - r0 : 32);
-        int32_t rrow = 0, ralen = 0;
-        int64_t rab = 0;
-        if (lane < nr) {
-            rrow = L.list ? __ldg(L.list + r0 + lane) : static_cast<int32_t>(r0 + lane);
-            rab = __ldg(L.a_rowptr + rrow);
-            ralen = static_cast<int32_t>(__ldg(L.a_rowptr + rrow + 1) - rab);
-        }
-        uint32_t todo = nr == 32 ? kFull : ((1u << nr) - 1u);
-        auto pop = [&]() {
-            const int q = todo ? __ffs(todo) - 1 : -1;
-            todo &= todo - 1;
-            return q;
-        };
-        auto s1 = [&](int q, int32_t& j) {
-            j = 0;
-            if (q < 0)
-                return;
-            const int32_t len = __shfl_sync(kFull, ralen, q);
-            const int64_t ab = __shfl_sync(kFull, rab, q);
-            if (len <= 32 && lane < len)
-                j = __ldg(L.a_cols + ab + lane);
-        };
-        auto s2 = [&](int q, int32_t j, int64_t& bb, int32_t& bl) {
-            bb = 0;
-            bl = 0;
-            if (q < 0)
-                return;
-            const int32_t len = __shfl_sync(kFull, ralen, q);
-            if (len <= 32 && lane < len) {
-                bb = __ldg(b_rowptr + j);
-                bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
+        // (the pipelined short-row loop below is the kPipe instantiation)
+    } else {
+        // Short rows: taken 32 at a time and their dependent loads pipelined
+        // across rows (A entries two rows ahead, B-row descriptors one ahead;
+        // three register sets unrolled by three), as in numeric_lp_flat_kernel.
+        for (int64_t r0 = ((int64_t)blockIdx.x * L.wpb + wib) * 32; r0 < L.nrows; r0 += nwarps * 32) {
+            const int nr = static_cast<int>(L.nrows - r0 < 32 ? L.nrows - r0 : 32);
+            int32_t rrow = 0, ralen = 0;
+            int64_t rab = 0;
+            if (lane < nr) {
+                rrow = L.list ? __ldg(L.list + r0 + lane) : static_cast<int32_t>(r0 + lane);
+                rab = __ldg(L.a_rowptr + rrow);
+                ralen = static_cast<int32_t>(__ldg(L.a_rowptr + rrow + 1) - rab);
             }
-        };
-        auto s3 = [&](int q, int64_t bb, int32_t bl) {
-            const int32_t len = __shfl_sync(kFull, ralen, q);
-            const int32_t i = __shfl_sync(kFull, rrow, q);
-            if (len <= 32) {
-                const int64_t sz = direct_size(bb, bl);
-                if (sz >= 0) {
-                    if (lane == 0)
-                        L.sym_sizes[i] = sz;
+            uint32_t todo = nr == 32 ? kFull : ((1u << nr) - 1u);
+            auto pop = [&]() {
+                const int q = todo ? __ffs(todo) - 1 : -1;
+                todo &= todo - 1;
+                return q;
+            };
+            auto s1 = [&](int q, int32_t& j) {
+                j = 0;
+                if (q < 0)
                     return;
-                }
-                chunk(len, bb, bl);
-            } else {
+                const int32_t len = __shfl_sync(kFull, ralen, q);
                 const int64_t ab = __shfl_sync(kFull, rab, q);
-                for (int64_t p0 = ab; p0 < ab + len && !overflow; p0 += 32) {
-                    const int na = static_cast<int>(ab + len - p0 < 32 ? ab + len - p0 : 32);
-                    int64_t cbb = 0;
-                    int32_t cbl = 0;
-                    if (lane < na) {
-                        const int32_t jj = __ldg(L.a_cols + p0 + lane);
-                        cbb = __ldg(b_rowptr + jj);
-                        cbl = kCompressed ? __ldg(L.csize + jj) : static_cast<int32_t>(__ldg(b_rowptr + jj + 1) - cbb);
-                    }
-                    chunk(na, cbb, cbl);
+                if (len <= 32 && lane < len)
+                    j = __ldg(L.a_cols + ab + lane);
+            };
+            auto s2 = [&](int q, int32_t j, int64_t& bb, int32_t& bl) {
+                bb = 0;
+                bl = 0;
+                if (q < 0)
+                    return;
+                const int32_t len = __shfl_sync(kFull, ralen, q);
+                if (len <= 32 && lane < len) {
+                    bb = __ldg(b_rowptr + j);
+                    bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(b_rowptr + j + 1) - bb);
                 }
-            }
-            finish(i);
-        };
-        int32_t jA, jB, jC;
-        int64_t bA = 0, bB = 0, bC = 0;
-        int32_t lA = 0, lB = 0, lC = 0;
-        int qA = pop(), qB = pop(), qC = -1;
-        s1(qA, jA);
-        s1(qB, jB);
-        s2(qA, jA, bA, lA);
-        while (qA >= 0) {
-            qC = pop();
-            s1(qC, jC);
-            s2(qB, jB, bB, lB);
-            s3(qA, bA, lA);
-            if (qB < 0)
-                break;
-            qA = pop();
+            };
+            auto s3 = [&](int q, int64_t bb, int32_t bl) {
+                const int32_t len = __shfl_sync(kFull, ralen, q);
+                const int32_t i = __shfl_sync(kFull, rrow, q);
+                if (len <= 32) {
+                    const int64_t sz = direct_size(bb, bl);
+                    if (sz >= 0) {
+                        if (lane == 0)
+                            L.sym_sizes[i] = sz;
+                        return;
+                    }
+                    chunk(len, bb, bl);
+                } else {
+                    const int64_t ab = __shfl_sync(kFull, rab, q);
+                    for (int64_t p0 = ab; p0 < ab + len && !overflow; p0 += 32) {
+                        const int na = static_cast<int>(ab + len - p0 < 32 ? ab + len - p0 : 32);
+                        int64_t cbb = 0;
+                        int32_t cbl = 0;
+                        if (lane < na) {
+                            const int32_t jj = __ldg(L.a_cols + p0 + lane);
+                            cbb = __ldg(b_rowptr + jj);
+                            cbl = kCompressed ? __ldg(L.csize + jj) : static_cast<int32_t>(__ldg(b_rowptr + jj + 1) - cbb);
+                        }
+                        chunk(na, cbb, cbl);
+                    }
+                }
+                finish(i);
+            };
+            int32_t jA, jB, jC;
+            int64_t bA = 0, bB = 0, bC = 0;
+            int32_t lA = 0, lB = 0, lC = 0;
+            int qA = pop(), qB = pop(), qC = -1;
             s1(qA, jA);
-            s2(qC, jC, bC, lC);
-            s3(qB, bB, lB);
-            if (qC < 0)
-                break;
-            qB = pop();
             s1(qB, jB);
             s2(qA, jA, bA, lA);
-            s3(qC, bC, lC);
+            while (qA >= 0) {
+                qC = pop();
+                s1(qC, jC);
+                s2(qB, jB, bB, lB);
+                s3(qA, bA, lA);
+                if (qB < 0)
+                    break;
+                qA = pop();
+                s1(qA, jA);
+                s2(qC, jC, bC, lC);
+                s3(qB, bB, lB);
+                if (qC < 0)
+                    break;
+                qB = pop();
+                s1(qB, jB);
+                s2(qA, jA, bA, lA);
+                s3(qC, bC, lC);
+            }
         }
     }
 }

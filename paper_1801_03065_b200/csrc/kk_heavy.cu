@@ -307,7 +307,6 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
     __shared__ int32_t sh_warp[kHeavyWarps];
     __shared__ int64_t tile_lo[kHeavyWarps + 1];
     __shared__ int32_t next_bucket;
-    __shared__ int32_t s_total;
     __shared__ int64_t s_row;
     longlong2* srec = H.stage + (size_t)blockIdx.x * H.stage_cap;
 
@@ -346,10 +345,8 @@ __global__ void __launch_bounds__(kHeavyThreads) numeric_heavy_kernel(const RowL
         const int32_t before = block_excl_scan(mine, sh_warp, &F);
         if (F <= H.min_products || F > H.max_products)
             continue; // another launch (staging size class) takes this row
-        if (threadIdx.x == 0) {
-            s_total = F;
+        if (threadIdx.x == 0)
             next_bucket = 0;
-        }
         // tile w starts at the first A entry p whose product prefix P(p) >= F*w/8
         for (int w = 1; w < kHeavyWarps; ++w) {
             const int64_t target = static_cast<int64_t>(F) * w / kHeavyWarps;
