@@ -1118,7 +1118,8 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
         // Auto: heavy rows use the CTA dense-bitmap kernel when the column
         // domain (in 32-bit words) fits shared memory
         const int32_t dom_words = static_cast<int32_t>((int64_t{k} + 31) / 32);
-        const int32_t heavy_words = (sfast && dom_words <= kHeavySymWords) ? std::max(dom_words, 1) : 0;
+        // (domains wider than the bitmap are walked in ranges of kHeavySymWords words)
+        const int32_t heavy_words = sfast ? std::max(std::min(dom_words, kHeavySymWords), 1) : 0;
         auto sym_launch = [&](const PhaseClass& pc, const int32_t* list, int64_t nrows) {
             RowLaunch L{};
             L.a_rowptr = a->row_offsets;
@@ -1140,7 +1141,7 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             if (pc.l2 && heavy_words > 0) {
                 // heavy rows: CTA-wide dense bitmap over the column domain
                 const int grid = static_cast<int>(std::min<int64_t>(nrows, sm_count()));
-                cuda_check(launch_symbolic_heavy(L, S.variant == kVarSymCompressed, heavy_words, grid, st),
+                cuda_check(launch_symbolic_heavy(L, S.variant == kVarSymCompressed, heavy_words, std::max(dom_words, 1), grid, st),
                            "symbolic heavy kernel");
             } else if (pc.l2) {
                 ensure_pool(spool, S.l2, st);
@@ -1175,7 +1176,8 @@ int spg_symbolic(const spg_csr* a, const spg_csr* b, const spg_config* cfg_in, s
             L.sym_sizes = h->d_rowptr + 1;
             L.ctr = h->d_ctr;
             L.l1_keys = sym_l1_keys;
-            cuda_check(launch_symbolic_heavy(L, S.variant == kVarSymCompressed, heavy_words, sm_count(), st),
+            cuda_check(launch_symbolic_heavy(L, S.variant == kVarSymCompressed, heavy_words, std::max(dom_words, 1),
+                                             sm_count(), st),
                        "symbolic heavy kernel (retries)");
             cudaFreeAsync(d_retry_cnt, st);
             cudaFreeAsync(d_retry, st);

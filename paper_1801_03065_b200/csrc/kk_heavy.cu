@@ -144,7 +144,10 @@ __device__ __forceinline__ void walk_products(const RowLaunch& L, int64_t p_lo, 
 // symbolic: dense bitmap over the column domain, CTA per row
 // ---------------------------------------------------------------------------
 template <bool kCompressed>
-__global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L, int32_t words)
+// words: bitmap words in shared memory; dom_words: words of the whole column
+// domain.  A domain wider than the bitmap is walked in ranges of `words`
+// words, the row's pairs filtered per range (no size limit on k).
+__global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L, int32_t words, int32_t dom_words)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // bm: dense bitmap of the column domain; sm: one bit per bm word, set on
@@ -159,7 +162,11 @@ __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L,
     for (int t = threadIdx.x; t < words + swords; t += blockDim.x)
         bm[t] = 0u;
     __syncthreads();
+    int32_t r0 = 0; // first word of the current range
     auto add = [&](int32_t w, uint32_t word) {
+        w -= r0;
+        if (static_cast<uint32_t>(w) >= static_cast<uint32_t>(words))
+            return; // another range's word
         if (atomicOr(&bm[w], word) == 0u)
             atomicOr(&sm[w >> 5], 1u << (w & 31));
     };
@@ -167,71 +174,73 @@ __global__ void __launch_bounds__(1024) symbolic_heavy_kernel(const RowLaunch L,
     for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
         const int32_t i = L.list ? __ldg(L.list + r) : static_cast<int32_t>(r);
         const int64_t abeg = __ldg(L.a_rowptr + i), aend = __ldg(L.a_rowptr + i + 1);
-        // chunks of 32 A entries: a chunk with many products is split into
-        // 32-product windows over all warps, a small one goes to one warp
-        // (the union is order-free)
-        for (int64_t c = abeg, ci = 0; c < aend; c += 32, ++ci) {
-            const int na = static_cast<int>(aend - c < 32 ? aend - c : 32);
-            int64_t bb = 0;
-            int32_t bl = 0;
-            if (lane < na) {
-                const int32_t j = __ldg(L.a_cols + c + lane);
-                bb = __ldg(L.b_rowptr + j);
-                bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(L.b_rowptr + j + 1) - bb);
-            }
-            const int32_t tot = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<unsigned>(bl)));
-            const bool split = tot >= 8 * 32;
-            if (!split && (ci % nw) != warp)
-                continue;
-            HMap fm;
-            fm.init(bb, bl, 0.0, lane);
-            const int32_t w_first = split ? 32 * warp : 0, w_step = split ? 32 * nw : 32;
-            for (int32_t w0 = w_first; w0 < tot; w0 += w_step) {
-                // segments that start before the window (windows are strided)
-                fm.rank = __popc(__ballot_sync(kFull, lane < fm.nne && fm.cexcl < w0));
-                int32_t e;
-                int64_t base;
-                double a_unused;
-                fm.window(w0, lane, e, base, a_unused);
-                const int32_t t = w0 + lane;
-                if (t < tot) {
-                    const int64_t q = base + (t - e);
-                    if constexpr (kCompressed) {
-                        const int2 pr = __ldg(cpair + q);
-                        add(pr.x, static_cast<uint32_t>(pr.y));
-                    } else {
-                        const int32_t key = __ldg(L.b_cols + q);
-                        add(key >> 5, 1u << (key & 31));
+        unsigned long long row_cnt = 0; // (thread 0)
+        for (r0 = 0; r0 < dom_words; r0 += words) {
+            // chunks of 32 A entries: a chunk with many products is split into
+            // 32-product windows over all warps, a small one goes to one warp
+            // (the union is order-free)
+            for (int64_t c = abeg, ci = 0; c < aend; c += 32, ++ci) {
+                const int na = static_cast<int>(aend - c < 32 ? aend - c : 32);
+                int64_t bb = 0;
+                int32_t bl = 0;
+                if (lane < na) {
+                    const int32_t j = __ldg(L.a_cols + c + lane);
+                    bb = __ldg(L.b_rowptr + j);
+                    bl = kCompressed ? __ldg(L.csize + j) : static_cast<int32_t>(__ldg(L.b_rowptr + j + 1) - bb);
+                }
+                const int32_t tot = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<unsigned>(bl)));
+                const bool split = tot >= 8 * 32;
+                if (!split && (ci % nw) != warp)
+                    continue;
+                HMap fm;
+                fm.init(bb, bl, 0.0, lane);
+                const int32_t w_first = split ? 32 * warp : 0, w_step = split ? 32 * nw : 32;
+                for (int32_t w0 = w_first; w0 < tot; w0 += w_step) {
+                    // segments that start before the window (windows are strided)
+                    fm.rank = __popc(__ballot_sync(kFull, lane < fm.nne && fm.cexcl < w0));
+                    int32_t e;
+                    int64_t base;
+                    double a_unused;
+                    fm.window(w0, lane, e, base, a_unused);
+                    const int32_t t = w0 + lane;
+                    if (t < tot) {
+                        const int64_t q = base + (t - e);
+                        if constexpr (kCompressed) {
+                            const int2 pr = __ldg(cpair + q);
+                            add(pr.x, static_cast<uint32_t>(pr.y));
+                        } else {
+                            const int32_t key = __ldg(L.b_cols + q);
+                            add(key >> 5, 1u << (key & 31));
+                        }
                     }
                 }
             }
-        }
-        __syncthreads();
-        unsigned long long cnt = 0;
-        for (int t = threadIdx.x; t < swords; t += blockDim.x) {
-            uint32_t sw = sm[t];
-            while (sw) {
-                const int b = __ffs(sw) - 1;
-                sw &= sw - 1;
-                const int32_t w = (t << 5) + b;
-                cnt += __popc(bm[w]);
-                bm[w] = 0u;
+            __syncthreads();
+            unsigned long long cnt = 0;
+            for (int t = threadIdx.x; t < swords; t += blockDim.x) {
+                uint32_t sw = sm[t];
+                while (sw) {
+                    const int b = __ffs(sw) - 1;
+                    sw &= sw - 1;
+                    const int32_t w = (t << 5) + b;
+                    cnt += __popc(bm[w]);
+                    bm[w] = 0u;
+                }
+                sm[t] = 0u;
             }
-            sm[t] = 0u;
-        }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1)
-            cnt += __shfl_xor_sync(kFull, cnt, off);
-        if (lane == 0)
-            red[warp] = cnt;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long s = 0;
-            for (int w = 0; w < nw; ++w)
-                s += red[w];
-            L.sym_sizes[i] = static_cast<int64_t>(s);
-        }
-        __syncthreads();
+    #pragma unroll
+            for (int off = 16; off >= 1; off >>= 1)
+                cnt += __shfl_xor_sync(kFull, cnt, off);
+            if (lane == 0)
+                red[warp] = cnt;
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int w = 0; w < nw; ++w)
+                    row_cnt += red[w];
+            __syncthreads();
+        } // column ranges
+        if (threadIdx.x == 0)
+            L.sym_sizes[i] = static_cast<int64_t>(row_cnt);
     }
 }
 
@@ -615,7 +624,8 @@ int numeric_heavy_blocks_per_sm(int32_t nb)
     return b > 0 ? b : 1;
 }
 
-cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st)
+cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int32_t dom_words, int grid,
+                                  cudaStream_t st)
 {
     if (L.nrows <= 0)
         return cudaSuccess;
@@ -626,9 +636,9 @@ cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t w
     if (e != cudaSuccess)
         return e;
     if (compressed)
-        symbolic_heavy_kernel<true><<<grid, 1024, smem, st>>>(L, words);
+        symbolic_heavy_kernel<true><<<grid, 1024, smem, st>>>(L, words, dom_words);
     else
-        symbolic_heavy_kernel<false><<<grid, 1024, smem, st>>>(L, words);
+        symbolic_heavy_kernel<false><<<grid, 1024, smem, st>>>(L, words, dom_words);
     count_launch();
     return cudaGetLastError();
 }

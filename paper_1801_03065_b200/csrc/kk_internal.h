@@ -138,7 +138,8 @@ cudaError_t launch_symbolic_fast(const RowLaunch& L, bool compressed, bool pipe,
 int symbolic_fast_blocks_per_sm(bool compressed, bool pipe, int wpb, size_t smem);
 
 // heavy rows (kk_heavy.cu)
-cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int grid, cudaStream_t st);
+cudaError_t launch_symbolic_heavy(const RowLaunch& L, bool compressed, int32_t words, int32_t dom_words, int grid,
+                                  cudaStream_t st);
 cudaError_t launch_numeric_heavy(const RowLaunch& L, void* stage, int64_t stage_cap,
                                  int32_t bucket_keys, int32_t nb, int64_t min_products, int64_t max_products,
                                  int queue, int grid, cudaStream_t st);

@@ -651,6 +651,39 @@ def test_heavy_row_beyond_half_a_million_outputs(kk, oracle):
     _sorted_parity(oracle, a, b, res.c.to_host())
 
 
+def test_heavy_rows_wide_column_domain(kk, oracle):
+    """k = 4M columns (125k bitmap words, wider than the heavy symbolic
+    kernel's 49,152-word shared bitmap): the heavy rows' union is walked in
+    column ranges, and the column slabs handle any k; bit-exact vs the oracle,
+    compressed and raw."""
+    rng = np.random.default_rng(71)
+    m, n, k = 6, 3000, 4_000_000
+
+    def wide(rows, cols, per_row):
+        ro = np.zeros(rows + 1, np.int64)
+        ci = []
+        for r in range(rows):
+            c = np.unique(rng.integers(0, cols, per_row))
+            ci.append(c.astype(np.int32))
+            ro[r + 1] = ro[r] + len(c)
+        ci = np.concatenate(ci)
+        return kk.CsrMatrix(rows, cols, ro, ci, rng.uniform(-1, 1, len(ci)), True)
+
+    a = wide(m, n, 300)
+    b = wide(n, k, 60)
+    for mode in (kk.CompressionMode.Always, kk.CompressionMode.Never):
+        res = kk.multiply(a, b, kk.SpgemmConfig(compression=mode))
+        assert res.handle.max_row_size > 8192  # rows beyond the warp tables
+        c = res.c.to_host()
+        ro = oracle.symbolic_row_offsets(a, b)
+        assert np.array_equal(c.row_offsets, ro)
+        cols, vals = oracle.numeric(a, b, ro)
+        sc, sv = oracle.sort_rows(ro, cols, vals)
+        gc, gv = oracle.sort_rows(ro, c.col_indices, c.values)
+        assert np.array_equal(sc, gc)
+        assert np.array_equal(sv.view(np.int64), gv.view(np.int64))
+
+
 def test_heavy_rows_unsorted_b(kk, oracle):
     """Unsorted B rows: the hashed-bucket heavy kernel; reusing a slab plan
     with an unsorted B of the same structure size raises instead of
