@@ -113,7 +113,10 @@ uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kWarpSmemMax = 48 * 1024; // L1 accumulator budget per warp
 constexpr double kTinyMaxAvgArow = 8.0;        // thread-per-row classes only for short A rows
-constexpr int32_t kHeavySymWords = 49152;     // 192 KB dense bitmap per CTA (heavy symbolic)
+#ifndef KK_HEAVY_SYM_WORDS
+#define KK_HEAVY_SYM_WORDS 49152
+#endif
+constexpr int32_t kHeavySymWords = KK_HEAVY_SYM_WORDS; // dense bitmap words per CTA (heavy symbolic)
 constexpr int32_t kHeavyBucketKeys = 256;     // numeric heavy rows: ~distinct columns per hashed bucket
 constexpr int32_t kHeavyMaxBuckets = 1536;    // buckets per row (shared-memory histogram bound)
 constexpr int64_t kHeavyMaxRow = int64_t{kHeavyMaxBuckets} * 320; // <= 62.5% load of the 512-slot tables
