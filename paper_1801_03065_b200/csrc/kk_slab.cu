@@ -2,12 +2,17 @@
 //
 // Rows of C beyond the warp tables (R-MAT squares: 10^3..5*10^5 outputs per
 // row, 10^4..10^7 products) are walked in column SLABS [c_lo, c_hi) sized so
-// that a slab's distinct columns fit one warp's shared-memory table (~600 of
-// 1024 slots).  B's rows are column-sorted, so the part of B row j inside a
-// slab is one contiguous RUN; per A entry the warp keeps a cursor (where the
-// next slab's run starts) and the column found there, so an A entry whose B
-// row has nothing in the slab costs one coalesced scratch read, and every
-// product is read exactly once.
+// that a slab's distinct columns fit one warp's shared-memory table (~225 of
+// 512 slots; 8 warps per CTA, 3 CTAs per SM).  B's rows are column-sorted, so
+// the part of B row j inside a slab is one contiguous RUN; per A entry the
+// warp keeps a cursor (where the next slab's run starts) and the column found
+// there, so an A entry whose B row has nothing in the slab costs one
+// coalesced scratch read, and every product is read exactly once.
+//
+// Plan: the cursors are scanned 32 at a time; entries with a run in the slab
+// go into a shared queue (A order) and their run ends are searched 32 queued
+// entries at a time.  Fold: a window producer keeps two mapped 32-product
+// windows (their B loads) in flight ahead of the window being folded.
 //
 // Left-to-right value order (bitwise the reference's sums): one
 // warp accumulates a slab, visiting its products in the reference's
