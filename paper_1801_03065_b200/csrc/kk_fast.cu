@@ -17,15 +17,19 @@
 //     lowest lane in lane (= product) order onto the running sum.  Rows are
 //     short and latency-bound, so a warp takes 32 rows at a time and
 //     pipelines their dependent loads across rows (A entries two rows ahead,
-//     B-row descriptors one row ahead).
+//     B-row descriptors one row ahead).  A row whose products fit one window
+//     skips the table: its key groups are the row's keys and the leaders'
+//     lane ranks their first-touch positions.
 //
 // symbolic_flat_kernel    Thread-Flat-Parallel structure union (engine.cpp:268-286
 //     with SymbolicSink :210-221) over the compressed graph (or raw columns).
 //     The union is order-independent, so duplicate keys inside a 32-product
 //     window are resolved with shared-memory CAS/OR instead of a warp fold,
 //     and the row size is the popcount of the table (no position bookkeeping).
-//     Tables are sized optimistically from the row bound; a row that overflows
-//     its table is re-queued to the exact-size path.  Chunks of very short
+//     Tables are sized optimistically from the row bound; a row whose probe
+//     sequence exceeds kSymMaxProbe (an over-full table) is re-queued to the
+//     exact-size path.  A row of at most 32 pairs skips the table (its size
+//     comes from the window's key groups).  Chunks of very short
 //     compressed rows run as segmented steps (several whole B rows per 32
 //     lanes); plans of short rows use the same row pipeline as the flat
 //     numeric kernel.
