@@ -67,7 +67,10 @@ constexpr int kTWMax = kTW * 3 / 4;                // keys before a slab is aban
 #define KK_SLAB_ACCEPT 1.6 // a planned slab predicted above ACCEPT * kX keys is re-planned narrower
 #endif
 constexpr int kX = kTW * KK_SLAB_XFRAC / 1024;     // target distinct keys per slab
-constexpr double kSplitWork = 4e8;  // A-row length x row size per part
+#ifndef KK_SLAB_SPLIT
+#define KK_SLAB_SPLIT 4e8
+#endif
+constexpr double kSplitWork = KK_SLAB_SPLIT; // A-row length x row size per part
 #ifndef KK_SLAB_DEPTH
 #define KK_SLAB_DEPTH 2 // mapped windows in flight ahead of the one being folded
 #endif
