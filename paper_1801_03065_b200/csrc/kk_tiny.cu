@@ -29,7 +29,10 @@ namespace kk {
 
 namespace {
 
-constexpr int kTinyThreads = 128;
+#ifndef KK_TINY_THREADS
+#define KK_TINY_THREADS 128
+#endif
+constexpr int kTinyThreads = KK_TINY_THREADS;
 
 __global__ void __launch_bounds__(kTinyThreads) numeric_tiny_kernel(const RowLaunch L)
 {
